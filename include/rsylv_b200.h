@@ -1,0 +1,140 @@
+/* rsylv-b200: B200-native (sm_100a) robust triangular Sylvester solver — C-ABI boundary.
+ *
+ * Solves  A*Y + Y*B = alpha*C  for upper quasi-triangular A (m x m) and B (n x n) in real
+ * Schur form (1x1 and 2x2 diagonal blocks), with every tile of Y kept below the overflow
+ * threshold omega through per-tile power-of-two scale factors (arXiv:1905.10574, Alg. 4).
+ *
+ * This header is the drop-in boundary for the reference entry point
+ *     rsylv::solve_tiled_robust(const QuasiTriangular& a, const QuasiTriangular& b,
+ *                               ConstMatrixView c, std::size_t tile_size,
+ *                               const OverflowConfig& cfg, ExecutionMode mode,
+ *                               const TileProbe& probe)
+ *   (/root/reference/proj/include/rsylv/tiled_solve.hpp:36-40, defined in
+ *    /root/reference/proj/src/tiled_solve.cpp:183-194).
+ * The C++ shim in shim/rsylv_b200_shim.cpp defines that exact symbol on top of this ABI and maps
+ * the status codes back to the reference exceptions (errors.hpp:10-37). Plain pointers and sizes
+ * only; matrices are column-major with a leading dimension exactly like ConstMatrixView
+ * (dense_matrix.hpp:12-30).
+ *
+ * Diagonal block structure (QuasiTriangular::diag_blocks, partition.hpp:15-42) is passed as one
+ * byte per index: blk[i] = 1 -> 1x1 block at i; 2 -> 2x2 block at (i, i+1); 0 -> second index
+ * of a 2x2 block. NULL means all 1x1.
+ */
+#ifndef RSYLV_B200_H
+#define RSYLV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. Reference exception each one maps to (errors.hpp, tiled_solve.cpp:187-188,
+ * partition.cpp:75-76, tile_grid.cpp:63-72, tiled_solve.cpp:77-79): */
+enum {
+    RSYLV_OK = 0,
+    RSYLV_INVALID_ARGUMENT = 1, /* std::invalid_argument                                      */
+    RSYLV_SINGULAR = 2,         /* SingularEquationError(pivot)                               */
+    RSYLV_SCALE_UNDERFLOW = 3,  /* ScaleUnderflowError: alpha < DBL_MIN. Y and alpha_exp are  */
+                                /* still returned (exponent form).                             */
+    RSYLV_CUDA_ERROR = 4,       /* device/runtime failure                                     */
+    RSYLV_NO_DEVICE = 5         /* no CUDA device / extension unusable: never a CPU fallback  */
+};
+
+/* Why an RSYLV_INVALID_ARGUMENT was raised (the reference's distinct throw sites). */
+enum {
+    RSYLV_REASON_NONE = 0,
+    RSYLV_REASON_NONCONFORMING = 1, /* tiled_solve.cpp:187-188 */
+    RSYLV_REASON_TILE_SIZE = 2,     /* partition.cpp:75-76      */
+    RSYLV_REASON_A_BOUND = 3,       /* tile_grid.cpp:63-64      */
+    RSYLV_REASON_B_BOUND = 4,       /* tile_grid.cpp:71-72      */
+    RSYLV_REASON_C_BOUND = 5,       /* tiled_solve.cpp:77-79    */
+    RSYLV_REASON_OPTIONS = 6
+};
+
+typedef struct {
+    double omega;      /* OverflowConfig::omega (overflow.hpp:15); 0 -> DBL_MAX/2           */
+    double small_num;  /* OverflowConfig::small_num (overflow.hpp:18); 0 -> DBL_MIN/eps      */
+    size_t tile_size;  /* requested tile size (>= 2); tiles above 1024 are split internally */
+    int scheduler;     /* 0: persistent dataflow kernel (default), 1: host-driven wavefront */
+    int reserved;
+} rsylv_b200_options;
+
+/* One TileProbe event (tiled_solve.hpp:24-27): tile (k, l) came to rest with local scale
+ * 2^scale_exp and cached inf-norm `norm`. */
+typedef struct {
+    uint32_t k, l;
+    int32_t scale_exp;
+    int32_t pad;
+    double norm;
+} rsylv_b200_probe_event;
+
+typedef struct {
+    double alpha;             /* 2^alpha_exp when >= DBL_MIN, else 0                        */
+    int32_t alpha_exp;        /* alpha as a power-of-two exponent (always set on OK/UNDERFLOW) */
+    int32_t invalid_reason;   /* RSYLV_REASON_*                                            */
+    uint64_t scaling_events;  /* guard activations (OverflowConfig::scaling_events)         */
+    double pivot;             /* offending pivot for RSYLV_SINGULAR                         */
+    double device_ms;         /* device time of the solve (pack .. unpack), CUDA events     */
+    double max_tile_norm;     /* max inf-norm over the returned tiles of Y (<= omega)       */
+    size_t row_tiles, col_tiles;
+    /* optional probe log: caller-owned buffer; probe_count receives the number of events
+     * produced (may exceed probe_cap; only the first probe_cap are written) */
+    rsylv_b200_probe_event* probe_log;
+    size_t probe_cap;
+    size_t probe_count;
+} rsylv_b200_result;
+
+typedef struct rsylv_b200_ctx rsylv_b200_ctx;
+
+/* Create a context on CUDA device `device` (0-based; -1 = current). */
+int rsylv_b200_create(int device, rsylv_b200_ctx** out);
+void rsylv_b200_destroy(rsylv_b200_ctx* ctx);
+const char* rsylv_b200_status_string(int status);
+/* Last CUDA error text of the context (for RSYLV_CUDA_ERROR). */
+const char* rsylv_b200_last_error(const rsylv_b200_ctx* ctx);
+
+/* Drop-in solve on HOST buffers (the reference's calling convention). Copies A, B, C to the
+ * device, solves, copies Y (m x n, leading dimension ldy) back. Replaces
+ * rsylv::solve_tiled_robust (tiled_solve.hpp:36-40). */
+int rsylv_b200_solve(rsylv_b200_ctx* ctx, size_t m, size_t n, const double* a, size_t lda,
+                     const unsigned char* ablk, const double* b, size_t ldb,
+                     const unsigned char* bblk, const double* c, size_t ldc, double* y,
+                     size_t ldy, const rsylv_b200_options* opt, rsylv_b200_result* res);
+
+/* Same solve on DEVICE-resident buffers (a, b, c, y are device pointers; ablk/bblk are host
+ * arrays). `stream` is a cudaStream_t (NULL = legacy default stream). */
+int rsylv_b200_solve_device(rsylv_b200_ctx* ctx, size_t m, size_t n, const double* a,
+                            size_t lda, const unsigned char* ablk, const double* b, size_t ldb,
+                            const unsigned char* bblk, const double* c, size_t ldc, double* y,
+                            size_t ldy, const rsylv_b200_options* opt, void* stream,
+                            rsylv_b200_result* res);
+
+/* One robust augmented-tile update <gamma,C> <- <gamma,C> - <alpha,A><beta,B>
+ * (rsylv::robust_update, robust_update.hpp:32-33) on the device, scales as exponents:
+ * gamma = 2^c_exp, alpha*beta = 2^ab_exp. C is m x n (ld m), A m x k, B k x n, HOST buffers.
+ * On return c holds the updated tile, *c_exp its new exponent and *c_norm its inf-norm. */
+int rsylv_b200_robust_update(rsylv_b200_ctx* ctx, size_t m, size_t k, size_t n, double* c,
+                             int32_t* c_exp, double* c_norm, const double* a, const double* b,
+                             int32_t ab_exp, double omega, uint64_t* events);
+
+/* ---- benchmark input generation (harness utility; not part of the reference API) ----
+ * Fills a device buffer (column-major, ld) with a quasi-triangular matrix whose strict upper
+ * triangle is U(up_lo, up_hi), 1x1 diagonal entries U(d_lo, d_hi) and 2x2 blocks
+ * [[a, b], [-c, a]] with a ~ U(d_lo, d_hi), b, c ~ U(off_lo, off_hi). Counter-based RNG keyed
+ * by (seed, i, j): identical on every device and run. */
+int rsylv_b200_generate_quasi_triangular(size_t n, double* dev, size_t ld,
+                                         const unsigned char* blk_host, uint64_t seed,
+                                         double up_lo, double up_hi, double d_lo, double d_hi,
+                                         double off_lo, double off_hi, void* stream);
+/* Dense m x n right-hand side: dist 0 = U(lo, hi), 1 = N(0, 1)*hi + lo. Tiles listed in
+ * hot_tiles (pairs of nominal tile indices of size hot_tile) are multiplied by hot_factor. */
+int rsylv_b200_generate_rhs(size_t m, size_t n, double* dev, size_t ld, uint64_t seed, int dist,
+                            double lo, double hi, const int32_t* hot_tiles, size_t n_hot,
+                            size_t hot_tile, double hot_factor, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,163 @@
+// rsylv-b200 device-side common definitions (sm_100a).
+//
+// Scale factors are powers of two kept as int32 exponents, so every rescale is exact and no
+// local scale can underflow mid-solve (the reference keeps doubles in (0,1] and throws
+// ScaleUnderflowError from accumulate_scale, overflow.cpp:42-46). Growth bounds that the
+// reference evaluates in x87 long double (overflow.cpp:29-57, robust_update.cpp:36-39) are
+// evaluated here in mantissa/exponent form ("xf"), which cannot overflow.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rsb {
+
+constexpr int kSub = 32;         // sub-block edge inside a diagonal-tile solve (<= warp width)
+constexpr int kSubMax = 34;      // max sub-blocks per tile edge (tile <= 1024, sub-blocks >= 31)
+constexpr int kTileMax = 1024;   // largest internal tile edge
+constexpr int kBM = 128;         // update-task subtile edge (rows and cols)
+constexpr int kKC = 32;          // K depth of one pipeline stage
+constexpr int kStages = 3;       // cp.async pipeline depth
+constexpr int kThreads = 512;    // 16 warps, for both task kinds
+constexpr int kWarps = kThreads / 32;
+constexpr int kLDA = kBM + 4;    // smem A stage: [kKC][kLDA] (rows contiguous), conflict-free
+constexpr int kLDB = kKC + 4;    // smem B stage: [kBM][kLDB] (k contiguous), conflict-free
+constexpr int kLDW = 33;         // per-warp sub-block buffer leading dim
+
+// error codes written to the device error word (first writer wins)
+enum : int { kErrNone = 0, kErrSingular = 2, kErrInternal = 9 };
+
+// ---------------------------------------------------------------------------------------
+// xf: nonnegative value m * 2^e with m in [0.5, 1), or zero (m == 0).
+struct xf {
+    double m;
+    int e;
+};
+
+__host__ __device__ __forceinline__ xf xf_zero() { return {0.0, 0}; }
+
+__host__ __device__ __forceinline__ xf xf_from(double v) {
+    int e = 0;
+    double m = frexp(v, &e);
+    if (v == 0.0) return {0.0, 0};
+    return {m, e};
+}
+
+__host__ __device__ __forceinline__ xf xf_renorm(double m, int e) {
+    if (m == 0.0) return {0.0, 0};
+    int d = 0;
+    double mm = frexp(m, &d);
+    return {mm, e + d};
+}
+
+__host__ __device__ __forceinline__ xf xf_mul(xf a, xf b) {
+    if (a.m == 0.0 || b.m == 0.0) return {0.0, 0};
+    return xf_renorm(a.m * b.m, a.e + b.e);
+}
+
+__host__ __device__ __forceinline__ xf xf_shift(xf a, int k) {
+    if (a.m == 0.0) return a;
+    return {a.m, a.e + k};
+}
+
+// Upper-bound-preserving sum: a difference of more than ~1074 binades drops the smaller term,
+// an error far inside the 2^-30 shave headroom (overflow.cpp:17).
+__host__ __device__ __forceinline__ xf xf_add(xf a, xf b) {
+    if (a.m == 0.0) return b;
+    if (b.m == 0.0) return a;
+    if (a.e < b.e) {
+        xf t = a;
+        a = b;
+        b = t;
+    }
+    const int d = a.e - b.e;
+    const double s = d > 1080 ? a.m : a.m + ldexp(b.m, -d);
+    return xf_renorm(s, a.e);
+}
+
+__host__ __device__ __forceinline__ bool xf_le(xf a, xf b) {
+    if (a.m == 0.0) return true;
+    if (b.m == 0.0) return false;
+    if (a.e != b.e) return a.e < b.e;
+    return a.m <= b.m;
+}
+
+__host__ __device__ __forceinline__ xf xf_max(xf a, xf b) { return xf_le(a, b) ? b : a; }
+
+// Power-of-two guard (the exponent form of update_scale, overflow.cpp:29-40): 0 when
+// g <= omega; otherwise the least d >= 1 with g * 2^-d <= target (= omega * (1 - 2^-30)).
+__host__ __device__ __forceinline__ int xf_guard(xf g, xf omega, xf target) {
+    if (xf_le(g, omega)) return 0;
+    int d = g.e - target.e + (g.m > target.m ? 1 : 0);
+    return d < 1 ? 1 : d;
+}
+
+__host__ __device__ __forceinline__ double xf_to_double(xf a) { return ldexp(a.m, a.e); }
+
+// 2^e as a double for e in [-1022, 1023] (exact, no libm call).
+__host__ __device__ __forceinline__ double pow2(int e) {
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double((long long)(e + 1023) << 52);
+#else
+    return ldexp(1.0, e);
+#endif
+}
+
+// x * 2^e for any e (two steps outside the normal exponent range).
+__host__ __device__ __forceinline__ double scale2(double x, int e) {
+    if (e >= -1022 && e <= 1023) return x * pow2(e);
+    if (e < -1022) {
+        if (e < -2100) return x * 0.0;
+        return (x * pow2(-1022)) * pow2(e + 1022);
+    }
+    if (e > 2046) return x * pow2(1023) * pow2(1023);
+    return (x * pow2(1023)) * pow2(e - 1023);
+}
+
+// ---------------------------------------------------------------------------------------
+// Problem descriptor shared by all kernels (device pointers unless noted).
+struct ProbeEv {
+    unsigned int k, l;
+    int scale_exp;
+    int pad;
+    double norm;
+};
+
+struct Problem {
+    int M, N;       // row / column tile counts
+    int TSP;        // packed tile slot leading dimension (multiple of kBM)
+    int m, n;
+    const int* rcut;            // M+1 row-tile cuts
+    const int* ccut;            // N+1 col-tile cuts
+    const unsigned char* ablk;  // m block codes
+    const unsigned char* bblk;  // n block codes
+    const double* Apack;        // upper tiles of A, slot tri(i,k) = k*(k+1)/2 + i
+    const double* Bpack;        // upper tiles of B
+    double* Ypack;              // all tiles of Y, slot i*N + j
+    double* anorm;              // M*M, (i,k) at i*M+k (upper)
+    double* bnorm;              // N*N, (l,j) at l*N+j (upper)
+    double* ynorm;              // M*N current cached tile norm
+    int* yexp;                  // M*N tile exponent (scale = 2^yexp, yexp <= 0)
+    int* uexp;                  // M*N exponent after the update phase
+    double* ubnd;               // M*N update-phase growth bound (cached norm at rest)
+    int* state;                 // M*N: 1 once solved (persistent scheduler flags)
+    int* udone;                 // M*N: finished update subtasks
+    int* err;                   // first error code
+    double* err_pivot;
+    unsigned long long* events; // scaling events
+    ProbeEv* probe;             // optional probe log
+    unsigned long long* probe_count;
+    unsigned long long probe_cap;
+    int* task_next;             // persistent scheduler: next task index
+    const int* tasks;           // persistent scheduler: packed (i, j, sr, sc) task list
+    int ntasks;
+    int nsub_r, nsub_c;         // subtiles per tile edge (TSP / kBM)
+    double omega, small_num;
+    xf x_omega, x_target;       // omega and omega * (1 - 2^-30) in xf form
+};
+
+__host__ __device__ __forceinline__ long long tri_slot(int i, int k) {
+    return (long long)k * (k + 1) / 2 + i;
+}
+
+}  // namespace rsb

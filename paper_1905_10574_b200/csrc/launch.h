@@ -1,0 +1,30 @@
+// Host-side declarations of the kernel launch wrappers defined in kernels.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace rsb {
+
+size_t smem_update();
+size_t smem_solve();
+size_t smem_persistent();
+cudaError_t configure_kernels();
+
+void launch_pack_upper(const double* src, long long ld, const int* cut, int T, int TSP,
+                       double* dst, double* norms, cudaStream_t st);
+void launch_pack_full(const double* src, long long ld, const Problem& P, double* norms,
+                      cudaStream_t st);
+void launch_update_diag(const Problem& P, int d, int ntiles, cudaStream_t st);
+void launch_solve_diag(const Problem& P, int d, int ntiles, cudaStream_t st);
+void launch_persistent(const Problem& P, int grid, cudaStream_t st);
+void launch_unpack(const Problem& P, int alpha_exp, double* y, long long ldy, cudaStream_t st);
+void launch_gen_qt(int n, double* a, long long ld, const unsigned char* blk,
+                   unsigned long long seed, double up_lo, double up_hi, double d_lo, double d_hi,
+                   double off_lo, double off_hi, cudaStream_t st);
+void launch_gen_rhs(int m, int n, double* c, long long ld, unsigned long long seed, int dist,
+                    double lo, double hi, const int* hot, int nhot, int hot_tile,
+                    double hot_factor, cudaStream_t st);
+
+}  // namespace rsb

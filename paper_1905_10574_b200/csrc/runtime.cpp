@@ -1,0 +1,605 @@
+// rsylv-b200 host runtime: the C-ABI of include/rsylv_b200.h.
+//
+// Host-side orchestration of the tiled robust solve (reference: tiled_solve.cpp:183-194 and
+// the TileGrid of tile_grid.cpp): argument validation in the reference's order, tile
+// partitioning, device workspace management, kernel launches (persistent dataflow scheduler or
+// host-driven wavefront), the alpha reduction (tile_grid.cpp:38-42) and the final verdict.
+#include <cfloat>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/rsylv_b200.h"
+#include "launch.h"
+
+using namespace rsb;
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+
+}  // namespace
+
+struct rsylv_b200_ctx {
+    int device = 0;
+    int sms = 0;
+    cudaStream_t own_stream = nullptr;
+    std::map<std::string, DevBuf> bufs;
+    std::string last_error;
+    bool configured = false;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // cached task list of the persistent scheduler
+    std::vector<int> tasks_host;
+    std::string tasks_key;
+};
+
+namespace {
+
+struct Fail {
+    int status;
+};
+
+void ck(rsylv_b200_ctx* ctx, cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        ctx->last_error = std::string(what) + ": " + cudaGetErrorString(e);
+        throw Fail{RSYLV_CUDA_ERROR};
+    }
+}
+
+template <class T>
+T* buf(rsylv_b200_ctx* ctx, const char* name, size_t count) {
+    DevBuf& b = ctx->bufs[name];
+    const size_t bytes = count * sizeof(T) + 256;
+    if (b.cap < bytes) {
+        if (b.p) cudaFree(b.p);
+        b.p = nullptr;
+        b.cap = 0;
+        ck(ctx, cudaMalloc(&b.p, bytes), name);
+        b.cap = bytes;
+    }
+    return static_cast<T*>(b.p);
+}
+
+// Tile partition: cut at running multiples of ts; a cut that would split a 2x2 block moves
+// one index EARLIER (the reference moves it later, partition.cpp:74-91; Y/alpha does not depend
+// on the partition and earlier cuts keep every tile within one padded slot).
+std::vector<int> partition(const unsigned char* blk, size_t n, size_t ts) {
+    std::vector<int> cuts{0};
+    size_t pos = 0;
+    while (pos < n) {
+        size_t nx = pos + ts;
+        if (nx >= n)
+            nx = n;
+        else if (blk && blk[nx - 1] == 2)
+            --nx;
+        cuts.push_back((int)nx);
+        pos = nx;
+    }
+    return cuts;
+}
+
+xf host_xf(double v) { return xf_from(v); }
+
+struct SolveArgs {
+    size_t m, n;
+    const double *a, *b, *c;
+    size_t lda, ldb, ldc;
+    const unsigned char *ablk, *bblk;
+    double* y;
+    size_t ldy;
+    rsylv_b200_options opt;
+    cudaStream_t st;
+    rsylv_b200_result* res;
+};
+
+std::vector<unsigned char> codes_or_ones(const unsigned char* blk, size_t n) {
+    std::vector<unsigned char> v(n, 1);
+    if (blk) std::memcpy(v.data(), blk, n);
+    return v;
+}
+
+int solve_device_impl(rsylv_b200_ctx* ctx, const SolveArgs& A) {
+    rsylv_b200_result* res = A.res;
+    const size_t m = A.m, n = A.n;
+    const double omega = A.opt.omega > 0 ? A.opt.omega : DBL_MAX / 2;
+    const double small_num = A.opt.small_num > 0 ? A.opt.small_num : DBL_MIN / DBL_EPSILON;
+    if (A.opt.tile_size < 2) {  // partition.cpp:75-76
+        res->invalid_reason = RSYLV_REASON_TILE_SIZE;
+        return RSYLV_INVALID_ARGUMENT;
+    }
+    if (m == 0 || n == 0) {
+        res->alpha = 1.0;
+        res->alpha_exp = 0;
+        return RSYLV_OK;
+    }
+    if (!ctx->configured) {
+        ck(ctx, configure_kernels(), "configure_kernels");
+        ctx->configured = true;
+    }
+    cudaStream_t st = A.st;
+    ck(ctx, cudaEventRecord(ctx->ev0, st), "event");
+
+    const size_t ts = A.opt.tile_size > (size_t)kTileMax ? (size_t)kTileMax : A.opt.tile_size;
+    std::vector<unsigned char> ac = codes_or_ones(A.ablk, m), bc = codes_or_ones(A.bblk, n);
+    std::vector<int> rc = partition(ac.data(), m, ts), cc = partition(bc.data(), n, ts);
+    const int M = (int)rc.size() - 1, N = (int)cc.size() - 1;
+    int tmax = 0;
+    for (int t = 0; t < M; ++t) tmax = std::max(tmax, rc[t + 1] - rc[t]);
+    for (int t = 0; t < N; ++t) tmax = std::max(tmax, cc[t + 1] - cc[t]);
+    const int TSP = (tmax + kBM - 1) / kBM * kBM;
+    const size_t slot = (size_t)TSP * TSP;
+    const size_t slack = (size_t)64 * TSP + 1024;
+    const size_t na = (size_t)M * (M + 1) / 2, nb = (size_t)N * (N + 1) / 2, ny = (size_t)M * N;
+    res->row_tiles = M;
+    res->col_tiles = N;
+
+    Problem P{};
+    P.M = M;
+    P.N = N;
+    P.TSP = TSP;
+    P.m = (int)m;
+    P.n = (int)n;
+    int* d_rc = buf<int>(ctx, "rcut", M + 1);
+    int* d_cc = buf<int>(ctx, "ccut", N + 1);
+    unsigned char* d_ab = buf<unsigned char>(ctx, "ablk", m);
+    unsigned char* d_bb = buf<unsigned char>(ctx, "bblk", n);
+    double* Ap = buf<double>(ctx, "Apack", na * slot + slack);
+    double* Bp = buf<double>(ctx, "Bpack", nb * slot + slack);
+    double* Yp = buf<double>(ctx, "Ypack", ny * slot + slack);
+    double* anorm = buf<double>(ctx, "anorm", (size_t)M * M);
+    double* bnorm = buf<double>(ctx, "bnorm", (size_t)N * N);
+    double* ynorm = buf<double>(ctx, "ynorm", ny);
+    int* yexp = buf<int>(ctx, "yexp", ny);
+    int* uexp = buf<int>(ctx, "uexp", ny);
+    double* ubnd = buf<double>(ctx, "ubnd", ny);
+    int* state = buf<int>(ctx, "state", ny);
+    int* udone = buf<int>(ctx, "udone", ny);
+    int* errw = buf<int>(ctx, "err", 4);
+    double* pivw = buf<double>(ctx, "pivot", 1);
+    unsigned long long* evw = buf<unsigned long long>(ctx, "events", 2);
+    int* tnext = buf<int>(ctx, "tnext", 1);
+    ck(ctx, cudaMemcpyAsync(d_rc, rc.data(), sizeof(int) * (M + 1), cudaMemcpyHostToDevice, st), "h2d");
+    ck(ctx, cudaMemcpyAsync(d_cc, cc.data(), sizeof(int) * (N + 1), cudaMemcpyHostToDevice, st), "h2d");
+    ck(ctx, cudaMemcpyAsync(d_ab, ac.data(), m, cudaMemcpyHostToDevice, st), "h2d");
+    ck(ctx, cudaMemcpyAsync(d_bb, bc.data(), n, cudaMemcpyHostToDevice, st), "h2d");
+    ck(ctx, cudaMemsetAsync(Ap + na * slot, 0, slack * sizeof(double), st), "memset");
+    ck(ctx, cudaMemsetAsync(Bp + nb * slot, 0, slack * sizeof(double), st), "memset");
+    ck(ctx, cudaMemsetAsync(Yp + ny * slot, 0, slack * sizeof(double), st), "memset");
+    ck(ctx, cudaMemsetAsync(errw, 0, 4 * sizeof(int), st), "memset");
+    ck(ctx, cudaMemsetAsync(evw, 0, 2 * sizeof(unsigned long long), st), "memset");
+    ck(ctx, cudaMemsetAsync(tnext, 0, sizeof(int), st), "memset");
+
+    P.rcut = d_rc;
+    P.ccut = d_cc;
+    P.ablk = d_ab;
+    P.bblk = d_bb;
+    P.Apack = Ap;
+    P.Bpack = Bp;
+    P.Ypack = Yp;
+    P.anorm = anorm;
+    P.bnorm = bnorm;
+    P.ynorm = ynorm;
+    P.yexp = yexp;
+    P.uexp = uexp;
+    P.ubnd = ubnd;
+    P.state = state;
+    P.udone = udone;
+    P.err = errw;
+    P.err_pivot = pivw;
+    P.events = evw;
+    P.nsub_r = TSP / kBM;
+    P.nsub_c = TSP / kBM;
+    P.omega = omega;
+    P.small_num = small_num;
+    P.x_omega = host_xf(omega);
+    P.x_target = host_xf(omega * (1.0 - 0x1p-30));
+    P.task_next = tnext;
+
+    rsylv_b200_probe_event* d_probe = nullptr;
+    unsigned long long* d_pc = evw + 1;
+    if (res->probe_log && res->probe_cap) {
+        d_probe = buf<rsylv_b200_probe_event>(ctx, "probe", res->probe_cap);
+        P.probe = reinterpret_cast<ProbeEv*>(d_probe);
+        P.probe_count = d_pc;
+        P.probe_cap = res->probe_cap;
+    }
+
+    // ---- TileGrid + compute_bounds: pack tiles and their norms (one HBM pass)
+    launch_pack_upper(A.a, (long long)A.lda, d_rc, M, TSP, Ap, anorm, st);
+    launch_pack_upper(A.b, (long long)A.ldb, d_cc, N, TSP, Bp, bnorm, st);
+    launch_pack_full(A.c, (long long)A.ldc, P, ynorm, st);
+    ck(ctx, cudaGetLastError(), "pack");
+
+    // ---- validation in the reference order (tile_grid.cpp:59-74, tiled_solve.cpp:74-80)
+    std::vector<double> h_an((size_t)M * M), h_bn((size_t)N * N), h_yn(ny);
+    ck(ctx, cudaMemcpyAsync(h_an.data(), anorm, sizeof(double) * M * M, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(ctx, cudaMemcpyAsync(h_bn.data(), bnorm, sizeof(double) * N * N, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(ctx, cudaMemcpyAsync(h_yn.data(), ynorm, sizeof(double) * ny, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(ctx, cudaStreamSynchronize(st), "sync");
+    for (int i = 0; i < M; ++i)
+        for (int k = i; k < M; ++k)
+            if (!(h_an[(size_t)i * M + k] <= omega)) {
+                res->invalid_reason = RSYLV_REASON_A_BOUND;
+                return RSYLV_INVALID_ARGUMENT;
+            }
+    for (int l = 0; l < N; ++l)
+        for (int j = l; j < N; ++j)
+            if (!(h_bn[(size_t)l * N + j] <= omega)) {
+                res->invalid_reason = RSYLV_REASON_B_BOUND;
+                return RSYLV_INVALID_ARGUMENT;
+            }
+    for (size_t t = 0; t < ny; ++t)
+        if (!(h_yn[t] <= omega)) {
+            res->invalid_reason = RSYLV_REASON_C_BOUND;
+            return RSYLV_INVALID_ARGUMENT;
+        }
+
+    // ---- the tile DAG
+    if (A.opt.scheduler == 1) {
+        for (int d = 0; d <= M + N - 2; ++d) {
+            const int jlo = std::max(0, d - (M - 1)), jhi = std::min(N - 1, d);
+            const int nt = jhi - jlo + 1;
+            if (d > 0) launch_update_diag(P, d, nt, st);
+            launch_solve_diag(P, d, nt, st);
+        }
+        ck(ctx, cudaGetLastError(), "wavefront");
+    } else {
+        std::string key = std::to_string(M) + "/" + std::to_string(N) + "/" + std::to_string(TSP);
+        for (int v : rc) key += "," + std::to_string(v);
+        key += "|";
+        for (int v : cc) key += "," + std::to_string(v);
+        if (ctx->tasks_key != key) {
+            std::vector<int>& T = ctx->tasks_host;
+            T.clear();
+            for (int d = 0; d <= M + N - 2; ++d) {
+                const int jlo = std::max(0, d - (M - 1)), jhi = std::min(N - 1, d);
+                for (int j = jlo; j <= jhi; ++j) {
+                    const int i = M - 1 - d + j;
+                    const int nr = (rc[i + 1] - rc[i] + kBM - 1) / kBM;
+                    const int ncs = (cc[j + 1] - cc[j] + kBM - 1) / kBM;
+                    for (int sr = 0; sr < nr; ++sr)
+                        for (int sc = 0; sc < ncs; ++sc) {
+                            T.push_back(i);
+                            T.push_back(j);
+                            T.push_back(sr);
+                            T.push_back(sc);
+                        }
+                }
+            }
+            ctx->tasks_key = key;
+            int* d_tasks = buf<int>(ctx, "tasks", T.size());
+            ck(ctx, cudaMemcpyAsync(d_tasks, T.data(), sizeof(int) * T.size(),
+                                    cudaMemcpyHostToDevice, st), "h2d");
+        }
+        P.tasks = buf<int>(ctx, "tasks", ctx->tasks_host.size());
+        P.ntasks = (int)(ctx->tasks_host.size() / 4);
+        launch_persistent(P, ctx->sms, st);
+        ck(ctx, cudaGetLastError(), "persistent");
+    }
+
+    // ---- alpha reduction (tile_grid.cpp:38-42) in exponent form + joint renormalisation
+    std::vector<int> h_ye(ny);
+    int h_err[4];
+    double h_piv = 0;
+    unsigned long long h_ev[2];
+    ck(ctx, cudaMemcpyAsync(h_ye.data(), yexp, sizeof(int) * ny, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(ctx, cudaMemcpyAsync(h_yn.data(), ynorm, sizeof(double) * ny, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(ctx, cudaMemcpyAsync(h_err, errw, sizeof h_err, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(ctx, cudaMemcpyAsync(&h_piv, pivw, sizeof h_piv, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(ctx, cudaMemcpyAsync(h_ev, evw, sizeof h_ev, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(ctx, cudaStreamSynchronize(st), "solve");
+    res->scaling_events = h_ev[0];
+    if (d_probe) {
+        res->probe_count = (size_t)h_ev[1];
+        const size_t nc = std::min(res->probe_count, res->probe_cap);
+        ck(ctx, cudaMemcpy(res->probe_log, d_probe, nc * sizeof(rsylv_b200_probe_event),
+                           cudaMemcpyDeviceToHost), "d2h");
+    }
+    if (h_err[0] != 0) {
+        res->pivot = h_piv;
+        return h_err[0] == kErrSingular ? RSYLV_SINGULAR : RSYLV_CUDA_ERROR;
+    }
+    int emin = 0;
+    for (size_t t = 0; t < ny; ++t) emin = std::min(emin, h_ye[t]);
+    double numax = 0.0;
+    for (size_t t = 0; t < ny; ++t) numax = std::max(numax, std::ldexp(h_yn[t], emin - h_ye[t]));
+    // largest s >= 0 with numax * 2^s <= omega and emin + s <= 0
+    int s = -emin;
+    if (numax > 0.0) {
+        int en = 0, eo = 0;
+        const double mn = std::frexp(numax, &en), mo = std::frexp(omega, &eo);
+        const int smax = eo - en - (mn <= mo ? 0 : 1);
+        s = std::max(0, std::min(s, smax));
+    }
+    const int alpha_exp = emin + s;
+    res->alpha_exp = alpha_exp;
+    res->alpha = alpha_exp >= -1022 ? std::ldexp(1.0, alpha_exp) : 0.0;
+    res->max_tile_norm = std::ldexp(numax, s);
+
+    // ---- consistency scaling fused with the copy-out (tile_grid.cpp:44-52)
+    launch_unpack(P, alpha_exp, A.y, (long long)A.ldy, st);
+    ck(ctx, cudaGetLastError(), "unpack");
+    ck(ctx, cudaEventRecord(ctx->ev1, st), "event");
+    ck(ctx, cudaEventSynchronize(ctx->ev1), "sync");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    res->device_ms = ms;
+    return alpha_exp >= -1022 ? RSYLV_OK : RSYLV_SCALE_UNDERFLOW;
+}
+
+int guarded_call(rsylv_b200_ctx* ctx, int (*fn)(rsylv_b200_ctx*, const SolveArgs&),
+                 const SolveArgs& a) {
+    try {
+        return fn(ctx, a);
+    } catch (const Fail& f) {
+        return f.status;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rsylv_b200_status_string(int s) {
+    switch (s) {
+        case RSYLV_OK: return "ok";
+        case RSYLV_INVALID_ARGUMENT: return "invalid_argument";
+        case RSYLV_SINGULAR: return "SingularEquationError";
+        case RSYLV_SCALE_UNDERFLOW: return "ScaleUnderflowError";
+        case RSYLV_CUDA_ERROR: return "cuda_error";
+        case RSYLV_NO_DEVICE: return "no_device";
+        default: return "unknown";
+    }
+}
+
+const char* rsylv_b200_last_error(const rsylv_b200_ctx* ctx) {
+    return ctx ? ctx->last_error.c_str() : "";
+}
+
+int rsylv_b200_create(int device, rsylv_b200_ctx** out) {
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return RSYLV_NO_DEVICE;
+    if (device < 0) cudaGetDevice(&device);
+    if (device >= count) return RSYLV_NO_DEVICE;
+    if (cudaSetDevice(device) != cudaSuccess) return RSYLV_NO_DEVICE;
+    auto* ctx = new rsylv_b200_ctx();
+    ctx->device = device;
+    cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
+    if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) {
+        delete ctx;
+        return RSYLV_CUDA_ERROR;
+    }
+    *out = ctx;
+    return RSYLV_OK;
+}
+
+void rsylv_b200_destroy(rsylv_b200_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    for (auto& kv : ctx->bufs)
+        if (kv.second.p) cudaFree(kv.second.p);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+}
+
+static void init_result(rsylv_b200_result* r) {
+    rsylv_b200_probe_event* log = r->probe_log;
+    size_t cap = r->probe_cap;
+    std::memset(r, 0, sizeof *r);
+    r->probe_log = log;
+    r->probe_cap = cap;
+}
+
+int rsylv_b200_solve_device(rsylv_b200_ctx* ctx, size_t m, size_t n, const double* a,
+                            size_t lda, const unsigned char* ablk, const double* b, size_t ldb,
+                            const unsigned char* bblk, const double* c, size_t ldc, double* y,
+                            size_t ldy, const rsylv_b200_options* opt, void* stream,
+                            rsylv_b200_result* res) {
+    if (!ctx || !opt || !res) return RSYLV_INVALID_ARGUMENT;
+    init_result(res);
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return RSYLV_CUDA_ERROR;
+    SolveArgs A{m, n, a, b, c, lda, ldb, ldc, ablk, bblk, y, ldy, *opt,
+                stream ? (cudaStream_t)stream : ctx->own_stream, res};
+    return guarded_call(ctx, solve_device_impl, A);
+}
+
+static int solve_host_impl(rsylv_b200_ctx* ctx, const SolveArgs& H) {
+    cudaStream_t st = H.st;
+    const size_t m = H.m, n = H.n;
+    double* da = buf<double>(ctx, "hA", m * m);
+    double* db = buf<double>(ctx, "hB", n * n);
+    double* dc = buf<double>(ctx, "hC", m * n);
+    double* dy = buf<double>(ctx, "hY", m * n);
+    ck(ctx, cudaMemcpy2DAsync(da, m * 8, H.a, H.lda * 8, m * 8, m, cudaMemcpyHostToDevice, st), "h2d A");
+    ck(ctx, cudaMemcpy2DAsync(db, n * 8, H.b, H.ldb * 8, n * 8, n, cudaMemcpyHostToDevice, st), "h2d B");
+    ck(ctx, cudaMemcpy2DAsync(dc, m * 8, H.c, H.ldc * 8, m * 8, n, cudaMemcpyHostToDevice, st), "h2d C");
+    SolveArgs D = H;
+    D.a = da;
+    D.b = db;
+    D.c = dc;
+    D.y = dy;
+    D.lda = m;
+    D.ldb = n;
+    D.ldc = m;
+    D.ldy = m;
+    const int status = solve_device_impl(ctx, D);
+    if (status == RSYLV_OK || status == RSYLV_SCALE_UNDERFLOW) {
+        ck(ctx, cudaMemcpy2DAsync(H.y, H.ldy * 8, dy, m * 8, m * 8, n, cudaMemcpyDeviceToHost, st), "d2h Y");
+        ck(ctx, cudaStreamSynchronize(st), "sync");
+    }
+    return status;
+}
+
+int rsylv_b200_solve(rsylv_b200_ctx* ctx, size_t m, size_t n, const double* a, size_t lda,
+                     const unsigned char* ablk, const double* b, size_t ldb,
+                     const unsigned char* bblk, const double* c, size_t ldc, double* y,
+                     size_t ldy, const rsylv_b200_options* opt, rsylv_b200_result* res) {
+    if (!ctx || !opt || !res) return RSYLV_INVALID_ARGUMENT;
+    init_result(res);
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return RSYLV_CUDA_ERROR;
+    if (opt->tile_size < 2) {
+        res->invalid_reason = RSYLV_REASON_TILE_SIZE;
+        return RSYLV_INVALID_ARGUMENT;
+    }
+    if (m == 0 || n == 0) {
+        res->alpha = 1.0;
+        return RSYLV_OK;
+    }
+    SolveArgs A{m, n, a, b, c, lda, ldb, ldc, ablk, bblk, y, ldy, *opt, ctx->own_stream, res};
+    return guarded_call(ctx, solve_host_impl, A);
+}
+
+int rsylv_b200_robust_update(rsylv_b200_ctx* ctx, size_t m, size_t k, size_t n, double* c,
+                             int32_t* c_exp, double* c_norm, const double* a, const double* b,
+                             int32_t ab_exp, double omega, uint64_t* events) {
+    if (!ctx || m == 0 || k == 0 || n == 0 || m > kTileMax || k > kTileMax || n > kTileMax)
+        return RSYLV_INVALID_ARGUMENT;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return RSYLV_CUDA_ERROR;
+    try {
+        if (!ctx->configured) {
+            ck(ctx, configure_kernels(), "configure_kernels");
+            ctx->configured = true;
+        }
+        cudaStream_t st = ctx->own_stream;
+        // embed the update as column update Y_00 -= A_01 * Y_10 of a 2 x 1 tile grid
+        const size_t mk = m + k;
+        std::vector<double> abig(mk * mk, 0.0), ybig(mk * n, 0.0);
+        for (size_t j = 0; j < k; ++j)
+            for (size_t i = 0; i < m; ++i) abig[i + (m + j) * mk] = a[i + j * m];
+        for (size_t j = 0; j < mk; ++j) abig[j + j * mk] = 1.0;
+        for (size_t j = 0; j < n; ++j) {
+            for (size_t i = 0; i < m; ++i) ybig[i + j * mk] = c[i + j * m];
+            for (size_t i = 0; i < k; ++i) ybig[m + i + j * mk] = b[i + j * k];
+        }
+        const int M = 2, N = 1;
+        std::vector<int> rc{0, (int)m, (int)mk}, cc{0, (int)n};
+        const int tmax = (int)std::max(std::max(m, k), n);
+        const int TSP = (tmax + kBM - 1) / kBM * kBM;
+        const size_t slot = (size_t)TSP * TSP, slack = (size_t)64 * TSP + 1024;
+        double* dA = buf<double>(ctx, "ruA", mk * mk);
+        double* dY = buf<double>(ctx, "ruY", mk * n);
+        double* Ap = buf<double>(ctx, "ruApack", 3 * slot + slack);
+        double* Bp = buf<double>(ctx, "ruBpack", 1 * slot + slack);
+        double* Yp = buf<double>(ctx, "ruYpack", 2 * slot + slack);
+        double* an = buf<double>(ctx, "ruan", 4);
+        double* bn = buf<double>(ctx, "rubn", 1);
+        double* yn = buf<double>(ctx, "ruyn", 2);
+        int* ye = buf<int>(ctx, "ruye", 2);
+        int* ue = buf<int>(ctx, "ruue", 2);
+        double* ub = buf<double>(ctx, "ruub", 2);
+        int* sta = buf<int>(ctx, "rust", 2);
+        int* ud = buf<int>(ctx, "ruud", 2);
+        int* errw = buf<int>(ctx, "ruerr", 4);
+        double* pivw = buf<double>(ctx, "rupiv", 1);
+        unsigned long long* evw = buf<unsigned long long>(ctx, "ruev", 2);
+        int* d_rc = buf<int>(ctx, "rurc", 3);
+        int* d_cc = buf<int>(ctx, "rucc", 2);
+        ck(ctx, cudaMemcpyAsync(dA, abig.data(), abig.size() * 8, cudaMemcpyHostToDevice, st), "h2d");
+        ck(ctx, cudaMemcpyAsync(dY, ybig.data(), ybig.size() * 8, cudaMemcpyHostToDevice, st), "h2d");
+        ck(ctx, cudaMemcpyAsync(d_rc, rc.data(), 12, cudaMemcpyHostToDevice, st), "h2d");
+        ck(ctx, cudaMemcpyAsync(d_cc, cc.data(), 8, cudaMemcpyHostToDevice, st), "h2d");
+        ck(ctx, cudaMemsetAsync(Ap, 0, (3 * slot + slack) * 8, st), "memset");
+        ck(ctx, cudaMemsetAsync(Bp, 0, (slot + slack) * 8, st), "memset");
+        ck(ctx, cudaMemsetAsync(Yp + 2 * slot, 0, slack * 8, st), "memset");
+        ck(ctx, cudaMemsetAsync(errw, 0, 16, st), "memset");
+        ck(ctx, cudaMemsetAsync(evw, 0, 16, st), "memset");
+        Problem P{};
+        P.M = M;
+        P.N = N;
+        P.TSP = TSP;
+        P.m = (int)mk;
+        P.n = (int)n;
+        P.rcut = d_rc;
+        P.ccut = d_cc;
+        P.Apack = Ap;
+        P.Bpack = Bp;
+        P.Ypack = Yp;
+        P.anorm = an;
+        P.bnorm = bn;
+        P.ynorm = yn;
+        P.yexp = ye;
+        P.uexp = ue;
+        P.ubnd = ub;
+        P.state = sta;
+        P.udone = ud;
+        P.err = errw;
+        P.err_pivot = pivw;
+        P.events = evw;
+        P.nsub_r = P.nsub_c = TSP / kBM;
+        P.omega = omega > 0 ? omega : DBL_MAX / 2;
+        P.small_num = DBL_MIN / DBL_EPSILON;
+        P.x_omega = host_xf(P.omega);
+        P.x_target = host_xf(P.omega * (1.0 - 0x1p-30));
+        launch_pack_upper(dA, (long long)mk, d_rc, M, TSP, Ap, an, st);
+        launch_pack_full(dY, (long long)mk, P, yn, st);
+        const int exps[2] = {c_exp ? *c_exp : 0, ab_exp};
+        ck(ctx, cudaMemcpyAsync(ye, exps, 8, cudaMemcpyHostToDevice, st), "h2d");
+        launch_update_diag(P, 1, 1, st);
+        ck(ctx, cudaGetLastError(), "update");
+        int ue_h = 0;
+        unsigned long long ev_h[2];
+        std::vector<double> out(slot);
+        ck(ctx, cudaMemcpyAsync(&ue_h, ue, 4, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(ctx, cudaMemcpyAsync(ev_h, evw, 16, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(ctx, cudaMemcpyAsync(out.data(), Yp, slot * 8, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(ctx, cudaStreamSynchronize(st), "sync");
+        double nrm = 0.0;
+        for (size_t i = 0; i < m; ++i) {
+            double s = 0.0;
+            for (size_t j = 0; j < n; ++j) {
+                c[i + j * m] = out[i + j * TSP];
+                s += std::fabs(c[i + j * m]);
+            }
+            nrm = std::max(nrm, s);
+        }
+        if (c_exp) *c_exp = ue_h;
+        if (c_norm) *c_norm = nrm;
+        if (events) *events = ev_h[0];
+        return RSYLV_OK;
+    } catch (const Fail& f) {
+        return f.status;
+    }
+}
+
+int rsylv_b200_generate_quasi_triangular(size_t n, double* dev, size_t ld,
+                                         const unsigned char* blk_host, uint64_t seed,
+                                         double up_lo, double up_hi, double d_lo, double d_hi,
+                                         double off_lo, double off_hi, void* stream) {
+    unsigned char* d_blk = nullptr;
+    if (blk_host) {
+        if (cudaMalloc(&d_blk, n) != cudaSuccess) return RSYLV_CUDA_ERROR;
+        cudaMemcpy(d_blk, blk_host, n, cudaMemcpyHostToDevice);
+    }
+    launch_gen_qt((int)n, dev, (long long)ld, d_blk, seed, up_lo, up_hi, d_lo, d_hi, off_lo,
+                  off_hi, (cudaStream_t)stream);
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (d_blk) cudaFree(d_blk);
+    return e == cudaSuccess ? RSYLV_OK : RSYLV_CUDA_ERROR;
+}
+
+int rsylv_b200_generate_rhs(size_t m, size_t n, double* dev, size_t ld, uint64_t seed, int dist,
+                            double lo, double hi, const int32_t* hot_tiles, size_t n_hot,
+                            size_t hot_tile, double hot_factor, void* stream) {
+    int* d_hot = nullptr;
+    if (n_hot) {
+        if (cudaMalloc(&d_hot, n_hot * 2 * sizeof(int)) != cudaSuccess) return RSYLV_CUDA_ERROR;
+        cudaMemcpy(d_hot, hot_tiles, n_hot * 2 * sizeof(int), cudaMemcpyHostToDevice);
+    }
+    launch_gen_rhs((int)m, (int)n, dev, (long long)ld, seed, dist, lo, hi, d_hot, (int)n_hot,
+                   (int)(hot_tile ? hot_tile : 1), hot_factor, (cudaStream_t)stream);
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (d_hot) cudaFree(d_hot);
+    return e == cudaSuccess ? RSYLV_OK : RSYLV_CUDA_ERROR;
+}
+
+}  // extern "C"
