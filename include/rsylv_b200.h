@@ -84,6 +84,11 @@ typedef struct {
     rsylv_b200_probe_event* probe_log;
     size_t probe_cap;
     size_t probe_count;
+    /* device-time breakdown (CUDA events on the solve stream) */
+    double pack_ms;           /* pack + tile norms (TileGrid + compute_bounds)               */
+    double dag_ms;            /* tile DAG: update GEMMs + diagonal solves                    */
+    double unpack_ms;         /* consistency scaling + copy-out                              */
+    uint64_t dag_launches;    /* kernel launches inside the DAG phase                        */
 } rsylv_b200_result;
 
 typedef struct rsylv_b200_ctx rsylv_b200_ctx;

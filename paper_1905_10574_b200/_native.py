@@ -36,7 +36,8 @@ class Result(C.Structure):
                 ("device_ms", C.c_double), ("max_tile_norm", C.c_double),
                 ("row_tiles", C.c_size_t), ("col_tiles", C.c_size_t),
                 ("probe_log", C.POINTER(ProbeEvent)), ("probe_cap", C.c_size_t),
-                ("probe_count", C.c_size_t)]
+                ("probe_count", C.c_size_t), ("pack_ms", C.c_double), ("dag_ms", C.c_double),
+                ("unpack_ms", C.c_double), ("dag_launches", C.c_uint64)]
 
 
 _dp = C.POINTER(C.c_double)

@@ -103,15 +103,12 @@ __host__ __device__ __forceinline__ double pow2(int e) {
 #endif
 }
 
-// x * 2^e for any e (two steps outside the normal exponent range).
+// x * 2^e for any e. Inside the normal exponent range one multiply (exact, or a single
+// rounding when the result is subnormal); outside it ldexp (single rounding). pow2(e) must only
+// ever see e in [-1022, 1023].
 __host__ __device__ __forceinline__ double scale2(double x, int e) {
     if (e >= -1022 && e <= 1023) return x * pow2(e);
-    if (e < -1022) {
-        if (e < -2100) return x * 0.0;
-        return (x * pow2(-1022)) * pow2(e + 1022);
-    }
-    if (e > 2046) return x * pow2(1023) * pow2(1023);
-    return (x * pow2(1023)) * pow2(e - 1023);
+    return ldexp(x, e);
 }
 
 // ---------------------------------------------------------------------------------------

@@ -33,7 +33,7 @@ struct rsylv_b200_ctx {
     std::map<std::string, DevBuf> bufs;
     std::string last_error;
     bool configured = false;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evp = nullptr, evd = nullptr;
     // cached task list of the persistent scheduler
     std::vector<int> tasks_host;
     std::string tasks_key;
@@ -241,12 +241,15 @@ int solve_device_impl(rsylv_b200_ctx* ctx, const SolveArgs& A) {
         }
 
     // ---- the tile DAG
+    ck(ctx, cudaEventRecord(ctx->evp, st), "event");
     if (A.opt.scheduler == 1) {
+        res->dag_launches = 0;
         for (int d = 0; d <= M + N - 2; ++d) {
             const int jlo = std::max(0, d - (M - 1)), jhi = std::min(N - 1, d);
             const int nt = jhi - jlo + 1;
             if (d > 0) launch_update_diag(P, d, nt, st);
             launch_solve_diag(P, d, nt, st);
+            res->dag_launches += d > 0 ? 2 : 1;
         }
         ck(ctx, cudaGetLastError(), "wavefront");
     } else {
@@ -281,7 +284,9 @@ int solve_device_impl(rsylv_b200_ctx* ctx, const SolveArgs& A) {
         P.ntasks = (int)(ctx->tasks_host.size() / 4);
         launch_persistent(P, ctx->sms, st);
         ck(ctx, cudaGetLastError(), "persistent");
+        res->dag_launches = 1;
     }
+    ck(ctx, cudaEventRecord(ctx->evd, st), "event");
 
     // ---- alpha reduction (tile_grid.cpp:38-42) in exponent form + joint renormalisation
     std::vector<int> h_ye(ny);
@@ -330,6 +335,12 @@ int solve_device_impl(rsylv_b200_ctx* ctx, const SolveArgs& A) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
     res->device_ms = ms;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->evp);
+    res->pack_ms = ms;
+    cudaEventElapsedTime(&ms, ctx->evp, ctx->evd);
+    res->dag_ms = ms;
+    cudaEventElapsedTime(&ms, ctx->evd, ctx->ev1);
+    res->unpack_ms = ms;
     return alpha_exp >= -1022 ? RSYLV_OK : RSYLV_SCALE_UNDERFLOW;
 }
 
@@ -373,7 +384,8 @@ int rsylv_b200_create(int device, rsylv_b200_ctx** out) {
     ctx->device = device;
     cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
     if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) {
+        cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
+        cudaEventCreate(&ctx->evp) != cudaSuccess || cudaEventCreate(&ctx->evd) != cudaSuccess) {
         delete ctx;
         return RSYLV_CUDA_ERROR;
     }
@@ -388,6 +400,8 @@ void rsylv_b200_destroy(rsylv_b200_ctx* ctx) {
         if (kv.second.p) cudaFree(kv.second.p);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->evp) cudaEventDestroy(ctx->evp);
+    if (ctx->evd) cudaEventDestroy(ctx->evd);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }
