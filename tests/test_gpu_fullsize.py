@@ -1,0 +1,66 @@
+"""BASELINE.json configurations at their literal sizes, on the GPU.
+
+* c1 (2000^2, the only config the reference can solve): Y vs the reference, run in parallel
+  mode on all host cores, norm-wise <= 1e-10 (north_star tolerance).
+* c2..c5: the reference throws ScaleUnderflowError (SURVEY.md finding 4: no normal-double alpha
+  exists). The GPU must complete in exponent form, return the same verdict through the API,
+  keep Y finite with every tile <= omega, and satisfy the size-independent property
+  A (Y x) + Y (B x) = alpha C x for random x (checked in a power-of-two prescaled frame).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+
+
+def projection_residual(torch, A, B, C, Y, alpha_exp, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    n = Y.shape[1]
+    x = torch.rand((n, 1), generator=g, dtype=torch.float64, device="cuda") - 0.5
+    ys = Y * 2.0 ** -24  # keep A*Y and Y*B finite (tiles are <= omega ~ 2^1023)
+    lhs = A @ (ys @ x) + ys @ (B @ x)
+    cx = C @ x
+    sh = alpha_exp - 24
+    rhs = torch.ldexp(cx, torch.tensor(sh, device="cuda")) if sh > -1074 else torch.zeros_like(cx)
+    r = torch.linalg.vector_norm(lhs - rhs)
+    den = (torch.linalg.matrix_norm(A) + torch.linalg.matrix_norm(B)) * \
+        torch.linalg.matrix_norm(ys) * torch.linalg.vector_norm(x) + torch.linalg.vector_norm(rhs)
+    return float(r / den)
+
+
+def solve_device(name, scheduler=0):
+    import torch
+    from paper_1905_10574_b200 import api
+    from paper_1905_10574_b200.configs import CONFIGS, device_system
+    cfg = CONFIGS[name]
+    A, ac, B, bc, C = device_system(cfg, torch)
+    Y = torch.empty((cfg.n, cfg.m), dtype=torch.float64, device="cuda").T
+    st, res = api.solve_tiled_robust_device(A, ac, B, bc, C, Y, cfg.tile, scheduler=scheduler,
+                                            raise_underflow=False)
+    return torch, cfg, A, ac, B, bc, C, Y, st, res
+
+
+def test_c1_full_vs_reference():
+    torch, cfg, A, ac, B, bc, C, Y, st, res = solve_device("c1")
+    assert st == 0 and res.alpha == 1.0
+    a, b, c = (t.cpu().numpy() for t in (A, B, C))
+    ref = po.solve_tiled(a, ac, b, bc, c, cfg.tile, impl="ref", workers=os.cpu_count() or 1)
+    assert ref.status == 0 and ref.alpha == 1.0
+    y = Y.cpu().numpy()
+    d = np.abs(y - ref.y).sum(axis=1).max() / np.abs(ref.y).sum(axis=1).max()
+    assert d <= 1e-10, d
+    assert projection_residual(torch, A, B, C, Y, 0) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+def test_literal_configs_complete_in_exponent_form(name):
+    torch, cfg, A, ac, B, bc, C, Y, st, res = solve_device(name)
+    assert st == 3, "reference verdict for this config is ScaleUnderflowError"
+    assert res.alpha_exp < -1022
+    assert bool(torch.isfinite(Y).all())
+    assert 0.0 < res.max_tile_norm <= np.finfo(float).max / 2
+    assert projection_residual(torch, A, B, C, Y, res.alpha_exp) <= 1e-12
