@@ -169,7 +169,7 @@ def solve_nonrobust(a, ablk, b, bblk, c, impl="oracle"):
 
 def robust_update(c, c_scale, c_norm, a, a_scale, a_norm, b, b_scale, b_norm, omega=0.0,
                   impl="oracle"):
-    c = _f(c).copy()
+    c = np.array(c, dtype=np.float64, order="F", copy=True)
     a, b = _f(a), _f(b)
     m, n = c.shape
     k = a.shape[1]

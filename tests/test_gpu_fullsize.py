@@ -21,10 +21,11 @@ def projection_residual(torch, A, B, C, Y, alpha_exp, seed=0):
     g = torch.Generator(device="cuda").manual_seed(seed)
     n = Y.shape[1]
     x = torch.rand((n, 1), generator=g, dtype=torch.float64, device="cuda") - 0.5
-    ys = Y * 2.0 ** -24  # keep A*Y and Y*B finite (tiles are <= omega ~ 2^1023)
+    # prescale by 2^-600 so that products and Frobenius squares stay finite (tiles <= 2^1023)
+    ys = Y * 2.0 ** -600
     lhs = A @ (ys @ x) + ys @ (B @ x)
     cx = C @ x
-    sh = alpha_exp - 24
+    sh = alpha_exp - 600
     rhs = torch.ldexp(cx, torch.tensor(sh, device="cuda")) if sh > -1074 else torch.zeros_like(cx)
     r = torch.linalg.vector_norm(lhs - rhs)
     den = (torch.linalg.matrix_norm(A) + torch.linalg.matrix_norm(B)) * \
