@@ -124,6 +124,10 @@ int rsylv_b200_robust_update(rsylv_b200_ctx* ctx, size_t m, size_t k, size_t n, 
                              int32_t* c_exp, double* c_norm, const double* a, const double* b,
                              int32_t ab_exp, double omega, uint64_t* events);
 
+/* Development counters: accumulated cycles per tile-task phase over all tasks since the last
+ * reset (0 update GEMM, 1 solve setup, 2 sub-block solves, 3 in-tile updates, 4 finalize). */
+int rsylv_b200_debug_counters(unsigned long long* out16, int reset);
+
 /* ---- benchmark input generation (harness utility; not part of the reference API) ----
  * Fills a device buffer (column-major, ld) with a quasi-triangular matrix whose strict upper
  * triangle is U(up_lo, up_hi), 1x1 diagonal entries U(d_lo, d_hi) and 2x2 blocks

@@ -12,20 +12,30 @@
 
 namespace rsb {
 
-constexpr int kSub = 32;         // sub-block edge inside a diagonal-tile solve (<= warp width)
-constexpr int kSubMax = 34;      // max sub-blocks per tile edge (tile <= 1024, sub-blocks >= 31)
-constexpr int kTileMax = 1024;   // largest internal tile edge
-constexpr int kBM = 128;         // update-task subtile edge (rows and cols)
+constexpr int kSub = 16;         // sub-block edge inside a diagonal-tile solve (<= warp width)
+constexpr int kBM = 128;         // internal tile edge: one CTA task owns one <= 128 x 128 tile
+constexpr int kTileMax = kBM;    // largest internal tile edge
+constexpr int kSubMax = 9;       // max sub-blocks per tile edge (tile <= 128, sub-blocks >= 15)
+constexpr int kLDT = kBM + 1;    // shared-memory tile leading dim (odd: conflict-free columns)
+constexpr int kLDD = kSub + 1;   // staged diagonal sub-block leading dim
 constexpr int kKC = 32;          // K depth of one pipeline stage
 constexpr int kStages = 3;       // cp.async pipeline depth
 constexpr int kThreads = 512;    // 16 warps, for both task kinds
 constexpr int kWarps = kThreads / 32;
 constexpr int kLDA = kBM + 4;    // smem A stage: [kKC][kLDA] (rows contiguous), conflict-free
 constexpr int kLDB = kKC + 4;    // smem B stage: [kBM][kLDB] (k contiguous), conflict-free
-constexpr int kLDW = 33;         // per-warp sub-block buffer leading dim
 
 // error codes written to the device error word (first writer wins)
 enum : int { kErrNone = 0, kErrSingular = 2, kErrInternal = 9 };
+
+// 2^e as a double for e in [-1022, 1023] (exact, no libm call).
+__host__ __device__ __forceinline__ double pow2(int e) {
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double((long long)(e + 1023) << 52);
+#else
+    return ldexp(1.0, e);
+#endif
+}
 
 // ---------------------------------------------------------------------------------------
 // xf: nonnegative value m * 2^e with m in [0.5, 1), or zero (m == 0).
@@ -36,18 +46,25 @@ struct xf {
 
 __host__ __device__ __forceinline__ xf xf_zero() { return {0.0, 0}; }
 
+// v >= 0 (finite, or +inf which maps to a value above every double)
 __host__ __device__ __forceinline__ xf xf_from(double v) {
-    int e = 0;
-    double m = frexp(v, &e);
+#ifdef __CUDA_ARCH__
+    const long long b = __double_as_longlong(v);
+    const int ex = (int)((b >> 52) & 0x7ff);
+    if (ex != 0 && ex != 0x7ff)
+        return {__longlong_as_double((b & 0x800fffffffffffffLL) | (1022LL << 52)), ex - 1022};
+    if (ex == 0x7ff) return {0.5, 1 << 20};
+#endif
     if (v == 0.0) return {0.0, 0};
+    int e = 0;
+    const double m = frexp(v, &e);
     return {m, e};
 }
 
 __host__ __device__ __forceinline__ xf xf_renorm(double m, int e) {
-    if (m == 0.0) return {0.0, 0};
-    int d = 0;
-    double mm = frexp(m, &d);
-    return {mm, e + d};
+    const xf t = xf_from(m);
+    if (t.m == 0.0) return t;
+    return {t.m, t.e + e};
 }
 
 __host__ __device__ __forceinline__ xf xf_mul(xf a, xf b) {
@@ -71,7 +88,7 @@ __host__ __device__ __forceinline__ xf xf_add(xf a, xf b) {
         b = t;
     }
     const int d = a.e - b.e;
-    const double s = d > 1080 ? a.m : a.m + ldexp(b.m, -d);
+    const double s = d > 1000 ? a.m : a.m + b.m * pow2(-d);
     return xf_renorm(s, a.e);
 }
 
@@ -93,15 +110,6 @@ __host__ __device__ __forceinline__ int xf_guard(xf g, xf omega, xf target) {
 }
 
 __host__ __device__ __forceinline__ double xf_to_double(xf a) { return ldexp(a.m, a.e); }
-
-// 2^e as a double for e in [-1022, 1023] (exact, no libm call).
-__host__ __device__ __forceinline__ double pow2(int e) {
-#ifdef __CUDA_ARCH__
-    return __longlong_as_double((long long)(e + 1023) << 52);
-#else
-    return ldexp(1.0, e);
-#endif
-}
 
 // x * 2^e for any e. Inside the normal exponent range one multiply (exact, or a single
 // rounding when the result is subnormal); outside it ldexp (single rounding). pow2(e) must only

@@ -7,17 +7,17 @@
 
 namespace rsb {
 
-size_t smem_update();
-size_t smem_solve();
-size_t smem_persistent();
+size_t smem_task();
+cudaError_t read_prof(unsigned long long* out);
+cudaError_t reset_prof();
 cudaError_t configure_kernels();
 
 void launch_pack_upper(const double* src, long long ld, const int* cut, int T, int TSP,
                        double* dst, double* norms, cudaStream_t st);
 void launch_pack_full(const double* src, long long ld, const Problem& P, double* norms,
                       cudaStream_t st);
-void launch_update_diag(const Problem& P, int d, int ntiles, cudaStream_t st);
-void launch_solve_diag(const Problem& P, int d, int ntiles, cudaStream_t st);
+void launch_tile_diag(const Problem& P, int d, int ntiles, cudaStream_t st);
+void launch_update_only(const Problem& P, int i, int j, cudaStream_t st);
 void launch_persistent(const Problem& P, int grid, cudaStream_t st);
 void launch_unpack(const Problem& P, int alpha_exp, double* y, long long ldy, cudaStream_t st);
 void launch_gen_qt(int n, double* a, long long ld, const unsigned char* blk,

@@ -247,9 +247,8 @@ int solve_device_impl(rsylv_b200_ctx* ctx, const SolveArgs& A) {
         for (int d = 0; d <= M + N - 2; ++d) {
             const int jlo = std::max(0, d - (M - 1)), jhi = std::min(N - 1, d);
             const int nt = jhi - jlo + 1;
-            if (d > 0) launch_update_diag(P, d, nt, st);
-            launch_solve_diag(P, d, nt, st);
-            res->dag_launches += d > 0 ? 2 : 1;
+            launch_tile_diag(P, d, nt, st);
+            res->dag_launches += 1;
         }
         ck(ctx, cudaGetLastError(), "wavefront");
     } else {
@@ -264,15 +263,8 @@ int solve_device_impl(rsylv_b200_ctx* ctx, const SolveArgs& A) {
                 const int jlo = std::max(0, d - (M - 1)), jhi = std::min(N - 1, d);
                 for (int j = jlo; j <= jhi; ++j) {
                     const int i = M - 1 - d + j;
-                    const int nr = (rc[i + 1] - rc[i] + kBM - 1) / kBM;
-                    const int ncs = (cc[j + 1] - cc[j] + kBM - 1) / kBM;
-                    for (int sr = 0; sr < nr; ++sr)
-                        for (int sc = 0; sc < ncs; ++sc) {
-                            T.push_back(i);
-                            T.push_back(j);
-                            T.push_back(sr);
-                            T.push_back(sc);
-                        }
+                    T.push_back(i);
+                    T.push_back(j);
                 }
             }
             ctx->tasks_key = key;
@@ -281,7 +273,7 @@ int solve_device_impl(rsylv_b200_ctx* ctx, const SolveArgs& A) {
                                     cudaMemcpyHostToDevice, st), "h2d");
         }
         P.tasks = buf<int>(ctx, "tasks", ctx->tasks_host.size());
-        P.ntasks = (int)(ctx->tasks_host.size() / 4);
+        P.ntasks = (int)(ctx->tasks_host.size() / 2);
         launch_persistent(P, ctx->sms, st);
         ck(ctx, cudaGetLastError(), "persistent");
         res->dag_launches = 1;
@@ -558,7 +550,7 @@ int rsylv_b200_robust_update(rsylv_b200_ctx* ctx, size_t m, size_t k, size_t n, 
         launch_pack_full(dY, (long long)mk, P, yn, st);
         const int exps[2] = {c_exp ? *c_exp : 0, ab_exp};
         ck(ctx, cudaMemcpyAsync(ye, exps, 8, cudaMemcpyHostToDevice, st), "h2d");
-        launch_update_diag(P, 1, 1, st);
+        launch_update_only(P, 0, 0, st);
         ck(ctx, cudaGetLastError(), "update");
         int ue_h = 0;
         unsigned long long ev_h[2];
@@ -583,6 +575,12 @@ int rsylv_b200_robust_update(rsylv_b200_ctx* ctx, size_t m, size_t k, size_t n, 
     } catch (const Fail& f) {
         return f.status;
     }
+}
+
+// development: per-phase cycle counters of the tile tasks (reset=1 clears them)
+int rsylv_b200_debug_counters(unsigned long long* out16, int reset) {
+    if (reset) return reset_prof() == cudaSuccess ? RSYLV_OK : RSYLV_CUDA_ERROR;
+    return read_prof(out16) == cudaSuccess ? RSYLV_OK : RSYLV_CUDA_ERROR;
 }
 
 int rsylv_b200_generate_quasi_triangular(size_t n, double* dev, size_t ld,

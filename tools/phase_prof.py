@@ -1,0 +1,22 @@
+"""Per-phase cycle counters of the tile tasks (development tool)."""
+import ctypes as C, sys, os
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
+import torch
+from paper_1905_10574_b200 import api, _native as nat
+from paper_1905_10574_b200.configs import CONFIGS, device_system
+L = nat.lib()
+L.rsylv_b200_debug_counters.argtypes = [C.POINTER(C.c_uint64), C.c_int]
+for name in sys.argv[1:] or ["c1"]:
+    cfg = CONFIGS[name]
+    A, ac, B, bc, Cm = device_system(cfg, torch)
+    Y = torch.empty((cfg.n, cfg.m), dtype=torch.float64, device="cuda").T
+    api.solve_tiled_robust_device(A, ac, B, bc, Cm, Y, cfg.tile, raise_underflow=False)
+    out = (C.c_uint64 * 16)()
+    L.rsylv_b200_debug_counters(out, 1)
+    st, res = api.solve_tiled_robust_device(A, ac, B, bc, Cm, Y, cfg.tile, raise_underflow=False)
+    L.rsylv_b200_debug_counters(out, 0)
+    ntiles = res.row_tiles * res.col_tiles
+    names = ["update", "setup", "subsolve", "in-tile upd", "finalize"]
+    tot = sum(out[i] for i in range(5))
+    print(name, "dag_ms", round(res.dag_ms, 2), "tiles", ntiles, " ".join(
+        f"{names[i]}={out[i] / ntiles / 1965:.1f}us({100 * out[i] / tot:.0f}%)" for i in range(5)))
