@@ -18,8 +18,9 @@ Inputs are 12.8 GB per matrix, far larger than the 126 MB L2, so no L2 flush is 
            /root/reference sources) on a bounded sample on this host's cores.
 
 --impl reference runs only the reference CPU path (rank 0) on that sample and prints its line.
-Multi-GPU (N > 1): one process per GPU (torchrun); every rank solves its own full replica of the
-problem (tile-column sharding is not implemented yet) and value aggregates over ranks.
+Multi-GPU (N > 1): one process per GPU (torchrun); tile columns block-cyclic over the ranks, solved
+tiles pushed to the consuming GPUs over NVLink (CUDA IPC), alpha via NCCL all-reduce MIN
+(paper_1905_10574_b200/dist.py). The problem size is fixed: strong scaling.
 """
 from __future__ import annotations
 
@@ -179,6 +180,11 @@ def main():
     ocfg = api.OverflowConfig()
 
     def step():
+        if world > 1:
+            from paper_1905_10574_b200.dist import solve_dist
+            st, _, res = solve_dist(A, ac, B, bc, Cm, Y, cfg.tile, ocfg, stream=stream.cuda_stream,
+                                    device=local)
+            return st, res
         st, res = api.solve_tiled_robust_device(A, ac, B, bc, Cm, Y, cfg.tile, ocfg,
                                                 stream=stream.cuda_stream,
                                                 scheduler=args.scheduler, device=local,
@@ -209,13 +215,17 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ms_step = ms / args.steps
-    value = cfg.flops() * world / (ms_step / 1e3) / 1e9
-    finite = bool(torch.isfinite(Y).all().item())
+    value = cfg.flops() / (ms_step / 1e3) / 1e9  # one solve per step, split over the ranks
+    if world > 1:
+        own = [j for j in range(0, (cfg.n + 127) // 128) if j % world == rank]
+        finite = all(bool(torch.isfinite(Y[:, j * 128:(j + 1) * 128]).all().item()) for j in own[:4])
+    else:
+        finite = bool(torch.isfinite(Y).all().item())
     alpha_exp = int(res.alpha_exp)
 
     # e2e through the host API with pinned buffers
     e2e = None
-    if not args.no_e2e and args.e2e_steps > 0:
+    if not args.no_e2e and args.e2e_steps > 0 and world == 1:
         # pinned host copies holding the column-major matrices (the storage of the .T views)
         hA = torch.empty((cfg.m, cfg.m), dtype=torch.float64, pin_memory=True)
         hB = torch.empty((cfg.n, cfg.n), dtype=torch.float64, pin_memory=True)
@@ -266,11 +276,13 @@ def main():
             "metric": "FP64 GFLOP/s (m*n*(m+n)) robust Sylvester solve",
             "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": {"workload": f"{cfg.name}: {cfg.note}", "m": cfg.m, "n": cfg.n,
                        "tile": cfg.tile, "scheduler": "persistent" if args.scheduler == 0
                        else "wavefront", "l2": "inputs 12.8 GB/matrix >> 126 MB L2, no flush",
-                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "parallelism": (f"tile columns block-cyclic over {world} GPUs, NVLink "
+                                       "tile push + NCCL alpha all-reduce") if world > 1 else "1 GPU",
                        "alpha_exp": alpha_exp, "status": nat.lib().rsylv_b200_status_string(
                            statuses[-1]).decode(), "y_finite": finite,
                        "scaling_events": int(res.scaling_events)},

@@ -58,7 +58,9 @@ typedef struct {
     double small_num;  /* OverflowConfig::small_num (overflow.hpp:18); 0 -> DBL_MIN/eps      */
     size_t tile_size;  /* requested tile size (>= 2); tiles above 1024 are split internally */
     int scheduler;     /* 0: persistent dataflow kernel (default), 1: host-driven wavefront */
-    int reserved;
+    int virtual_ranks; /* >1: emulate that many GPUs on this device (tile columns block-cyclic,
+                          solved tiles pushed between per-rank workspaces) -- validates the
+                          multi-GPU exchange on one GPU; 0/1 = off                          */
 } rsylv_b200_options;
 
 /* One TileProbe event (tiled_solve.hpp:24-27): tile (k, l) came to rest with local scale
@@ -116,6 +118,29 @@ int rsylv_b200_solve_device(rsylv_b200_ctx* ctx, size_t m, size_t n, const doubl
                             size_t ldy, const rsylv_b200_options* opt, void* stream,
                             rsylv_b200_result* res);
 
+/* ---- multi-GPU (one process per GPU; tile columns block-cyclic, column j on rank j % nranks).
+ * Sequence per solve (the caller provides the collectives, e.g. torch.distributed):
+ *   1. rsylv_b200_dist_prepare  : partition, allocate, pack, validate; writes this rank's IPC
+ *                                 handles (RSYLV_DIST_HANDLE_BYTES) for the peers
+ *   2. all-gather the handles; barrier (every rank packed before anyone pushes)
+ *   3. rsylv_b200_dist_run      : persistent kernel on the owned columns; solved tiles are pushed
+ *                                 over NVLink into the peers that consume them; returns the local
+ *                                 alpha exponent minimum (res->alpha_exp) and the local
+ *                                 max_tile_norm relative to it
+ *   4. all-reduce MIN / MAX of those two, then
+ *   5. rsylv_b200_dist_finish   : consistency scaling to the global alpha + copy-out of the
+ *                                 owned columns of Y (other columns are left untouched). */
+#define RSYLV_DIST_HANDLE_BYTES 320
+int rsylv_b200_dist_prepare(rsylv_b200_ctx* ctx, int nranks, int rank, size_t m, size_t n,
+                            const double* a, size_t lda, const unsigned char* ablk,
+                            const double* b, size_t ldb, const unsigned char* bblk,
+                            const double* c, size_t ldc, const rsylv_b200_options* opt,
+                            void* stream, void* handle_out, rsylv_b200_result* res);
+int rsylv_b200_dist_run(rsylv_b200_ctx* ctx, const void* all_handles, void* stream,
+                        rsylv_b200_result* res);
+int rsylv_b200_dist_finish(rsylv_b200_ctx* ctx, int alpha_exp, double* y, size_t ldy,
+                           void* stream, rsylv_b200_result* res);
+
 /* One robust augmented-tile update <gamma,C> <- <gamma,C> - <alpha,A><beta,B>
  * (rsylv::robust_update, robust_update.hpp:32-33) on the device, scales as exponents:
  * gamma = 2^c_exp, alpha*beta = 2^ab_exp. C is m x n (ld m), A m x k, B k x n, HOST buffers.
@@ -127,6 +152,8 @@ int rsylv_b200_robust_update(rsylv_b200_ctx* ctx, size_t m, size_t k, size_t n, 
 /* Development counters: accumulated cycles per tile-task phase over all tasks since the last
  * reset (0 update GEMM, 1 solve setup, 2 sub-block solves, 3 in-tile updates, 4 finalize). */
 int rsylv_b200_debug_counters(unsigned long long* out16, int reset);
+/* Development: average cycles of one warp-level 16x16 sub-block solve (mixed != 0: 2x2 blocks). */
+int rsylv_b200_debug_subsolve(int reps, int mixed, long long* cycles);
 
 /* ---- benchmark input generation (harness utility; not part of the reference API) ----
  * Fills a device buffer (column-major, ld) with a quasi-triangular matrix whose strict upper

@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(HERE, "librsylv_b200.so")
 
 RSYLV_OK, RSYLV_INVALID_ARGUMENT, RSYLV_SINGULAR, RSYLV_SCALE_UNDERFLOW = 0, 1, 2, 3
 RSYLV_CUDA_ERROR, RSYLV_NO_DEVICE = 4, 5
+DIST_HANDLE_BYTES = 320
 
 REASONS = {0: "", 1: "C does not conform with A and B", 2: "tile size must be >= 2",
            3: "a tile norm of A exceeds omega", 4: "a tile norm of B exceeds omega",
@@ -22,7 +23,7 @@ REASONS = {0: "", 1: "C does not conform with A and B", 2: "tile size must be >=
 
 class Options(C.Structure):
     _fields_ = [("omega", C.c_double), ("small_num", C.c_double), ("tile_size", C.c_size_t),
-                ("scheduler", C.c_int), ("reserved", C.c_int)]
+                ("scheduler", C.c_int), ("virtual_ranks", C.c_int)]
 
 
 class ProbeEvent(C.Structure):
@@ -68,6 +69,13 @@ def lib():
         L.rsylv_b200_robust_update.argtypes = [C.c_void_p, _sz, _sz, _sz, _dp,
                                                C.POINTER(C.c_int32), _dp, _dp, _dp, C.c_int32,
                                                C.c_double, C.POINTER(C.c_uint64)]
+        L.rsylv_b200_dist_prepare.argtypes = [C.c_void_p, C.c_int, C.c_int, _sz, _sz, C.c_void_p,
+                                              _sz, _up, C.c_void_p, _sz, _up, C.c_void_p, _sz,
+                                              C.POINTER(Options), C.c_void_p, C.c_void_p,
+                                              C.POINTER(Result)]
+        L.rsylv_b200_dist_run.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(Result)]
+        L.rsylv_b200_dist_finish.argtypes = [C.c_void_p, C.c_int, C.c_void_p, _sz, C.c_void_p,
+                                             C.POINTER(Result)]
         L.rsylv_b200_generate_quasi_triangular.argtypes = [_sz, C.c_void_p, _sz, _up,
                                                            C.c_uint64] + [C.c_double] * 6 + [
                                                                C.c_void_p]

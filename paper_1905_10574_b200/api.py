@@ -183,7 +183,7 @@ def solve_tiled_robust(a: QuasiTriangular, b: QuasiTriangular, c, tile_size: int
                        mode: Optional[ExecutionMode] = None,
                        probe: Optional[Callable[[int, int, float, float], None]] = None,
                        scheduler: int = 0, device: int = 0,
-                       probe_capacity: int = 1 << 20) -> SolveResult:
+                       probe_capacity: int = 1 << 20, virtual_ranks: int = 1) -> SolveResult:
     """Solves A*Y + Y*B = alpha*C with every tile of Y bounded by cfg.omega (tiled_solve.hpp:29-40).
 
     HOST arrays in, HOST array out (the reference calling convention). ``mode.workers`` is the
@@ -196,7 +196,7 @@ def solve_tiled_robust(a: QuasiTriangular, b: QuasiTriangular, c, tile_size: int
     m, n = c.shape
     cf = np.asfortranarray(c)
     y = np.zeros((m, n), order="F")
-    opt = nat.Options(cfg.omega, cfg.small_num, int(tile_size), scheduler, 0)
+    opt = nat.Options(cfg.omega, cfg.small_num, int(tile_size), scheduler, int(virtual_ranks))
     res = nat.Result()
     pbuf = None
     if probe is not None:
@@ -219,7 +219,8 @@ def solve_tiled_robust(a: QuasiTriangular, b: QuasiTriangular, c, tile_size: int
 
 def solve_tiled_robust_device(a_dev, a_codes, b_dev, b_codes, c_dev, y_dev, tile_size: int,
                               cfg: Optional[OverflowConfig] = None, stream=None,
-                              scheduler: int = 0, device: int = 0, raise_underflow=True):
+                              scheduler: int = 0, device: int = 0, raise_underflow=True,
+                              virtual_ranks: int = 1):
     """Device-resident variant: torch CUDA tensors (column-major, i.e. ``t.T.contiguous().T``
     or any tensor whose stride(0) == 1). Returns (status, nat.Result)."""
     cfg = cfg or OverflowConfig()
@@ -227,7 +228,7 @@ def solve_tiled_robust_device(a_dev, a_codes, b_dev, b_codes, c_dev, y_dev, tile
     for t in (a_dev, b_dev, c_dev, y_dev):
         if t.stride(0) != 1:
             raise ValueError("device arrays must be column-major (stride(0) == 1)")
-    opt = nat.Options(cfg.omega, cfg.small_num, int(tile_size), scheduler, 0)
+    opt = nat.Options(cfg.omega, cfg.small_num, int(tile_size), scheduler, int(virtual_ranks))
     res = nat.Result()
     up = lambda x: x.ctypes.data_as(C.POINTER(C.c_ubyte))  # noqa: E731
     st = nat.lib().rsylv_b200_solve_device(

@@ -18,6 +18,7 @@ constexpr int kTileMax = kBM;    // largest internal tile edge
 constexpr int kSubMax = 9;       // max sub-blocks per tile edge (tile <= 128, sub-blocks >= 15)
 constexpr int kLDT = kBM + 1;    // shared-memory tile leading dim (odd: conflict-free columns)
 constexpr int kLDD = kSub + 1;   // staged diagonal sub-block leading dim
+constexpr int kMaxRanks = 8;     // GPUs (or virtual ranks) sharing one solve
 constexpr int kKC = 32;          // K depth of one pipeline stage
 constexpr int kStages = 3;       // cp.async pipeline depth
 constexpr int kThreads = 512;    // 16 warps, for both task kinds
@@ -26,7 +27,8 @@ constexpr int kLDA = kBM + 4;    // smem A stage: [kKC][kLDA] (rows contiguous),
 constexpr int kLDB = kKC + 4;    // smem B stage: [kBM][kLDB] (k contiguous), conflict-free
 
 // error codes written to the device error word (first writer wins)
-enum : int { kErrNone = 0, kErrSingular = 2, kErrInternal = 9 };
+enum : int { kErrNone = 0, kErrSingular = 2, kErrWatchdog = 8, kErrInternal = 9 };
+constexpr unsigned long long kWatchdogNs = 60ull * 1000000000ull;  // a source tile never arriving
 
 // 2^e as a double for e in [-1022, 1023] (exact, no libm call).
 __host__ __device__ __forceinline__ double pow2(int e) {
@@ -159,6 +161,15 @@ struct Problem {
     int nsub_r, nsub_c;         // subtiles per tile edge (TSP / kBM)
     double omega, small_num;
     xf x_omega, x_target;       // omega and omega * (1 - 2^-30) in xf form
+    // multi-rank: tile columns block-cyclic over nranks (column j owned by rank j % nranks).
+    // Solved tiles are pushed into the peers' slots; peers are other GPUs (sys_scope = 1,
+    // CUDA-IPC-mapped pointers) or virtual ranks sharing one GPU (sys_scope = 0).
+    int nranks, rank, sys_scope;
+    double* peerY[kMaxRanks];
+    int* peerYexp[kMaxRanks];
+    double* peerYnorm[kMaxRanks];
+    int* peerState[kMaxRanks];
+    int* peerErr[kMaxRanks];
 };
 
 __host__ __device__ __forceinline__ long long tri_slot(int i, int k) {

@@ -8,6 +8,7 @@
 namespace rsb {
 
 size_t smem_task();
+int bench_subsolve(int reps, int mixed, long long* cycles_host);
 cudaError_t read_prof(unsigned long long* out);
 cudaError_t reset_prof();
 cudaError_t configure_kernels();
@@ -19,6 +20,8 @@ void launch_pack_full(const double* src, long long ld, const Problem& P, double*
 void launch_tile_diag(const Problem& P, int d, int ntiles, cudaStream_t st);
 void launch_update_only(const Problem& P, int i, int j, cudaStream_t st);
 void launch_persistent(const Problem& P, int grid, cudaStream_t st);
+cudaError_t launch_persistent_mr(const Problem* probs_dev, int nranks_here, int grid,
+                                 cudaStream_t st);
 void launch_unpack(const Problem& P, int alpha_exp, double* y, long long ldy, cudaStream_t st);
 void launch_gen_qt(int n, double* a, long long ld, const unsigned char* blk,
                    unsigned long long seed, double up_lo, double up_hi, double d_lo, double d_hi,

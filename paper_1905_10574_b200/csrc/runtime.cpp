@@ -34,9 +34,7 @@ struct rsylv_b200_ctx {
     std::string last_error;
     bool configured = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evp = nullptr, evd = nullptr;
-    // cached task list of the persistent scheduler
-    std::vector<int> tasks_host;
-    std::string tasks_key;
+    struct rsylv_b200_plan_holder* holder = nullptr;
 };
 
 namespace {
@@ -104,30 +102,88 @@ std::vector<unsigned char> codes_or_ones(const unsigned char* blk, size_t n) {
     return v;
 }
 
-int solve_device_impl(rsylv_b200_ctx* ctx, const SolveArgs& A) {
+// Per-rank device workspace (one per GPU; several per GPU in virtual-rank mode).
+struct RankBufs {
+    double* Yp = nullptr;
+    double* ynorm = nullptr;
+    int* yexp = nullptr;
+    int* uexp = nullptr;
+    double* ubnd = nullptr;
+    int* state = nullptr;
+    int* udone = nullptr;
+    int* err = nullptr;
+    double* piv = nullptr;
+    unsigned long long* ev = nullptr;
+    int* tnext = nullptr;
+    int* tasks = nullptr;
+    int ntasks = 0;
+};
+
+// Everything one solve needs between its phases (kept in the context for the dist_* calls).
+struct Plan {
+    int M = 0, N = 0, TSP = 0, nranks = 1;
+    size_t m = 0, n = 0, ny = 0;
+    double omega = 0, small_num = 0;
+    std::vector<int> rc, cc;
+    std::vector<int> local;        // ranks served by this process
+    std::vector<RankBufs> rb;      // one per local rank
+    Problem base{};
+    cudaStream_t st = nullptr;
+    int scheduler = 0;
+    rsylv_b200_probe_event* d_probe = nullptr;
+};
+
+}  // namespace
+
+struct rsylv_b200_plan_holder {
+    Plan plan;
+    std::vector<std::vector<unsigned char>> peer_handles;  // opened handle bytes per peer
+    std::vector<void*> peer_ptrs;                          // 5 per peer
+};
+
+namespace {
+
+rsylv_b200_plan_holder& ctx_holder(rsylv_b200_ctx* ctx) {
+    if (!ctx->holder) ctx->holder = new rsylv_b200_plan_holder();
+    return *ctx->holder;
+}
+Plan& ctx_plan(rsylv_b200_ctx* ctx) { return ctx_holder(ctx).plan; }
+
+void close_peers(rsylv_b200_ctx* ctx) {
+    rsylv_b200_plan_holder& H = ctx_holder(ctx);
+    for (void* p : H.peer_ptrs)
+        if (p) cudaIpcCloseMemHandle(p);
+    H.peer_ptrs.clear();
+    H.peer_handles.clear();
+}
+
+// Steps shared by every mode: partition (tile cut moved earlier around 2x2 blocks), device
+// workspaces, TileGrid + compute_bounds as one pack pass, validation in the reference order
+// (tile_grid.cpp:59-74, tiled_solve.cpp:74-80), per-rank task lists in anti-diagonal order.
+int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std::vector<int>& local) {
     rsylv_b200_result* res = A.res;
+    Plan& PL = ctx_plan(ctx);
     const size_t m = A.m, n = A.n;
-    const double omega = A.opt.omega > 0 ? A.opt.omega : DBL_MAX / 2;
-    const double small_num = A.opt.small_num > 0 ? A.opt.small_num : DBL_MIN / DBL_EPSILON;
-    if (A.opt.tile_size < 2) {  // partition.cpp:75-76
-        res->invalid_reason = RSYLV_REASON_TILE_SIZE;
-        return RSYLV_INVALID_ARGUMENT;
-    }
-    if (m == 0 || n == 0) {
-        res->alpha = 1.0;
-        res->alpha_exp = 0;
-        return RSYLV_OK;
-    }
+    PL.m = m;
+    PL.n = n;
+    PL.omega = A.opt.omega > 0 ? A.opt.omega : DBL_MAX / 2;
+    PL.small_num = A.opt.small_num > 0 ? A.opt.small_num : DBL_MIN / DBL_EPSILON;
+    PL.nranks = nranks;
+    PL.local = local;
+    PL.st = A.st;
+    PL.scheduler = A.opt.scheduler;
     if (!ctx->configured) {
         ck(ctx, configure_kernels(), "configure_kernels");
         ctx->configured = true;
     }
     cudaStream_t st = A.st;
     ck(ctx, cudaEventRecord(ctx->ev0, st), "event");
-
     const size_t ts = A.opt.tile_size > (size_t)kTileMax ? (size_t)kTileMax : A.opt.tile_size;
     std::vector<unsigned char> ac = codes_or_ones(A.ablk, m), bc = codes_or_ones(A.bblk, n);
-    std::vector<int> rc = partition(ac.data(), m, ts), cc = partition(bc.data(), n, ts);
+    PL.rc = partition(ac.data(), m, ts);
+    PL.cc = partition(bc.data(), n, ts);
+    const std::vector<int>& rc = PL.rc;
+    const std::vector<int>& cc = PL.cc;
     const int M = (int)rc.size() - 1, N = (int)cc.size() - 1;
     int tmax = 0;
     for (int t = 0; t < M; ++t) tmax = std::max(tmax, rc[t + 1] - rc[t]);
@@ -136,10 +192,15 @@ int solve_device_impl(rsylv_b200_ctx* ctx, const SolveArgs& A) {
     const size_t slot = (size_t)TSP * TSP;
     const size_t slack = (size_t)64 * TSP + 1024;
     const size_t na = (size_t)M * (M + 1) / 2, nb = (size_t)N * (N + 1) / 2, ny = (size_t)M * N;
+    PL.M = M;
+    PL.N = N;
+    PL.TSP = TSP;
+    PL.ny = ny;
     res->row_tiles = M;
     res->col_tiles = N;
 
-    Problem P{};
+    Problem& P = PL.base;
+    P = Problem{};
     P.M = M;
     P.N = N;
     P.TSP = TSP;
@@ -151,162 +212,255 @@ int solve_device_impl(rsylv_b200_ctx* ctx, const SolveArgs& A) {
     unsigned char* d_bb = buf<unsigned char>(ctx, "bblk", n);
     double* Ap = buf<double>(ctx, "Apack", na * slot + slack);
     double* Bp = buf<double>(ctx, "Bpack", nb * slot + slack);
-    double* Yp = buf<double>(ctx, "Ypack", ny * slot + slack);
     double* anorm = buf<double>(ctx, "anorm", (size_t)M * M);
     double* bnorm = buf<double>(ctx, "bnorm", (size_t)N * N);
-    double* ynorm = buf<double>(ctx, "ynorm", ny);
-    int* yexp = buf<int>(ctx, "yexp", ny);
-    int* uexp = buf<int>(ctx, "uexp", ny);
-    double* ubnd = buf<double>(ctx, "ubnd", ny);
-    int* state = buf<int>(ctx, "state", ny);
-    int* udone = buf<int>(ctx, "udone", ny);
-    int* errw = buf<int>(ctx, "err", 4);
-    double* pivw = buf<double>(ctx, "pivot", 1);
-    unsigned long long* evw = buf<unsigned long long>(ctx, "events", 2);
-    int* tnext = buf<int>(ctx, "tnext", 1);
     ck(ctx, cudaMemcpyAsync(d_rc, rc.data(), sizeof(int) * (M + 1), cudaMemcpyHostToDevice, st), "h2d");
     ck(ctx, cudaMemcpyAsync(d_cc, cc.data(), sizeof(int) * (N + 1), cudaMemcpyHostToDevice, st), "h2d");
     ck(ctx, cudaMemcpyAsync(d_ab, ac.data(), m, cudaMemcpyHostToDevice, st), "h2d");
     ck(ctx, cudaMemcpyAsync(d_bb, bc.data(), n, cudaMemcpyHostToDevice, st), "h2d");
     ck(ctx, cudaMemsetAsync(Ap + na * slot, 0, slack * sizeof(double), st), "memset");
     ck(ctx, cudaMemsetAsync(Bp + nb * slot, 0, slack * sizeof(double), st), "memset");
-    ck(ctx, cudaMemsetAsync(Yp + ny * slot, 0, slack * sizeof(double), st), "memset");
-    ck(ctx, cudaMemsetAsync(errw, 0, 4 * sizeof(int), st), "memset");
-    ck(ctx, cudaMemsetAsync(evw, 0, 2 * sizeof(unsigned long long), st), "memset");
-    ck(ctx, cudaMemsetAsync(tnext, 0, sizeof(int), st), "memset");
-
     P.rcut = d_rc;
     P.ccut = d_cc;
     P.ablk = d_ab;
     P.bblk = d_bb;
     P.Apack = Ap;
     P.Bpack = Bp;
-    P.Ypack = Yp;
     P.anorm = anorm;
     P.bnorm = bnorm;
-    P.ynorm = ynorm;
-    P.yexp = yexp;
-    P.uexp = uexp;
-    P.ubnd = ubnd;
-    P.state = state;
-    P.udone = udone;
-    P.err = errw;
-    P.err_pivot = pivw;
-    P.events = evw;
-    P.nsub_r = TSP / kBM;
-    P.nsub_c = TSP / kBM;
-    P.omega = omega;
-    P.small_num = small_num;
-    P.x_omega = host_xf(omega);
-    P.x_target = host_xf(omega * (1.0 - 0x1p-30));
-    P.task_next = tnext;
+    P.nsub_r = P.nsub_c = TSP / kBM;
+    P.omega = PL.omega;
+    P.small_num = PL.small_num;
+    P.x_omega = host_xf(PL.omega);
+    P.x_target = host_xf(PL.omega * (1.0 - 0x1p-30));
+    P.nranks = nranks;
 
-    rsylv_b200_probe_event* d_probe = nullptr;
-    unsigned long long* d_pc = evw + 1;
-    if (res->probe_log && res->probe_cap) {
-        d_probe = buf<rsylv_b200_probe_event>(ctx, "probe", res->probe_cap);
-        P.probe = reinterpret_cast<ProbeEv*>(d_probe);
-        P.probe_count = d_pc;
-        P.probe_cap = res->probe_cap;
-    }
-
-    // ---- TileGrid + compute_bounds: pack tiles and their norms (one HBM pass)
     launch_pack_upper(A.a, (long long)A.lda, d_rc, M, TSP, Ap, anorm, st);
     launch_pack_upper(A.b, (long long)A.ldb, d_cc, N, TSP, Bp, bnorm, st);
-    launch_pack_full(A.c, (long long)A.ldc, P, ynorm, st);
+
+    PL.rb.assign(local.size(), RankBufs{});
+    PL.d_probe = nullptr;
+    for (size_t li = 0; li < local.size(); ++li) {
+        const int r = local[li];
+        const std::string sfx = local.size() > 1 ? "#" + std::to_string(r) : std::string();
+        RankBufs& B = PL.rb[li];
+        B.Yp = buf<double>(ctx, ("Ypack" + sfx).c_str(), ny * slot + slack);
+        B.ynorm = buf<double>(ctx, ("ynorm" + sfx).c_str(), ny);
+        B.yexp = buf<int>(ctx, ("yexp" + sfx).c_str(), ny);
+        B.uexp = buf<int>(ctx, ("uexp" + sfx).c_str(), ny);
+        B.ubnd = buf<double>(ctx, ("ubnd" + sfx).c_str(), ny);
+        B.state = buf<int>(ctx, ("state" + sfx).c_str(), ny);
+        B.udone = buf<int>(ctx, ("udone" + sfx).c_str(), ny);
+        B.err = buf<int>(ctx, ("err" + sfx).c_str(), 4);
+        B.piv = buf<double>(ctx, ("pivot" + sfx).c_str(), 1);
+        B.ev = buf<unsigned long long>(ctx, ("events" + sfx).c_str(), 2);
+        B.tnext = buf<int>(ctx, ("tnext" + sfx).c_str(), 1);
+        ck(ctx, cudaMemsetAsync(B.Yp + ny * slot, 0, slack * sizeof(double), st), "memset");
+        ck(ctx, cudaMemsetAsync(B.err, 0, 4 * sizeof(int), st), "memset");
+        ck(ctx, cudaMemsetAsync(B.ev, 0, 2 * sizeof(unsigned long long), st), "memset");
+        ck(ctx, cudaMemsetAsync(B.tnext, 0, sizeof(int), st), "memset");
+        Problem Q = P;
+        Q.Ypack = B.Yp;
+        Q.ynorm = B.ynorm;
+        Q.yexp = B.yexp;
+        Q.uexp = B.uexp;
+        Q.state = B.state;
+        Q.udone = B.udone;
+        launch_pack_full(A.c, (long long)A.ldc, Q, B.ynorm, st);
+        // task list: owned tile columns, anti-diagonal order
+        std::vector<int> T;
+        for (int d = 0; d <= M + N - 2; ++d) {
+            const int jlo = std::max(0, d - (M - 1)), jhi = std::min(N - 1, d);
+            for (int j = jlo; j <= jhi; ++j) {
+                if (j % nranks != r) continue;
+                T.push_back(M - 1 - d + j);
+                T.push_back(j);
+            }
+        }
+        B.ntasks = (int)T.size() / 2;
+        B.tasks = buf<int>(ctx, ("tasks" + sfx).c_str(), T.size() + 2);
+        if (!T.empty())
+            ck(ctx, cudaMemcpyAsync(B.tasks, T.data(), sizeof(int) * T.size(), cudaMemcpyHostToDevice, st), "h2d");
+        ck(ctx, cudaStreamSynchronize(st), "sync");  // T goes out of scope
+    }
+    if (res->probe_log && res->probe_cap && nranks == 1)
+        PL.d_probe = buf<rsylv_b200_probe_event>(ctx, "probe", res->probe_cap);
     ck(ctx, cudaGetLastError(), "pack");
 
-    // ---- validation in the reference order (tile_grid.cpp:59-74, tiled_solve.cpp:74-80)
     std::vector<double> h_an((size_t)M * M), h_bn((size_t)N * N), h_yn(ny);
     ck(ctx, cudaMemcpyAsync(h_an.data(), anorm, sizeof(double) * M * M, cudaMemcpyDeviceToHost, st), "d2h");
     ck(ctx, cudaMemcpyAsync(h_bn.data(), bnorm, sizeof(double) * N * N, cudaMemcpyDeviceToHost, st), "d2h");
-    ck(ctx, cudaMemcpyAsync(h_yn.data(), ynorm, sizeof(double) * ny, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(ctx, cudaMemcpyAsync(h_yn.data(), PL.rb[0].ynorm, sizeof(double) * ny, cudaMemcpyDeviceToHost, st), "d2h");
     ck(ctx, cudaStreamSynchronize(st), "sync");
     for (int i = 0; i < M; ++i)
         for (int k = i; k < M; ++k)
-            if (!(h_an[(size_t)i * M + k] <= omega)) {
+            if (!(h_an[(size_t)i * M + k] <= PL.omega)) {
                 res->invalid_reason = RSYLV_REASON_A_BOUND;
                 return RSYLV_INVALID_ARGUMENT;
             }
     for (int l = 0; l < N; ++l)
         for (int j = l; j < N; ++j)
-            if (!(h_bn[(size_t)l * N + j] <= omega)) {
+            if (!(h_bn[(size_t)l * N + j] <= PL.omega)) {
                 res->invalid_reason = RSYLV_REASON_B_BOUND;
                 return RSYLV_INVALID_ARGUMENT;
             }
     for (size_t t = 0; t < ny; ++t)
-        if (!(h_yn[t] <= omega)) {
+        if (!(h_yn[t] <= PL.omega)) {
             res->invalid_reason = RSYLV_REASON_C_BOUND;
             return RSYLV_INVALID_ARGUMENT;
         }
+    return RSYLV_OK;
+}
 
-    // ---- the tile DAG
-    ck(ctx, cudaEventRecord(ctx->evp, st), "event");
-    if (A.opt.scheduler == 1) {
-        res->dag_launches = 0;
-        for (int d = 0; d <= M + N - 2; ++d) {
-            const int jlo = std::max(0, d - (M - 1)), jhi = std::min(N - 1, d);
-            const int nt = jhi - jlo + 1;
-            launch_tile_diag(P, d, nt, st);
-            res->dag_launches += 1;
+// Problem of local rank index li with its peers' pointers (virtual ranks: the other local
+// workspaces; distributed: IPC-mapped peer workspaces).
+Problem rank_problem(rsylv_b200_ctx* ctx, size_t li) {
+    Plan& PL = ctx_plan(ctx);
+    const RankBufs& B = PL.rb[li];
+    Problem Q = PL.base;
+    Q.Ypack = B.Yp;
+    Q.ynorm = B.ynorm;
+    Q.yexp = B.yexp;
+    Q.uexp = B.uexp;
+    Q.ubnd = B.ubnd;
+    Q.state = B.state;
+    Q.udone = B.udone;
+    Q.err = B.err;
+    Q.err_pivot = B.piv;
+    Q.events = B.ev;
+    Q.task_next = B.tnext;
+    Q.tasks = B.tasks;
+    Q.ntasks = B.ntasks;
+    Q.rank = PL.local[li];
+    Q.nranks = PL.nranks;
+    Q.sys_scope = 0;
+    if (PL.d_probe) {
+        Q.probe = reinterpret_cast<ProbeEv*>(PL.d_probe);
+        Q.probe_count = B.ev + 1;
+        Q.probe_cap = 0;
+    }
+    if (PL.nranks > 1) {
+        if (PL.local.size() > 1) {  // virtual ranks on this device
+            for (size_t lj = 0; lj < PL.local.size(); ++lj) {
+                const RankBufs& O = PL.rb[lj];
+                const int r = PL.local[lj];
+                Q.peerY[r] = O.Yp;
+                Q.peerYexp[r] = O.yexp;
+                Q.peerYnorm[r] = O.ynorm;
+                Q.peerState[r] = O.state;
+                Q.peerErr[r] = O.err;
+            }
+        } else {  // one rank per GPU
+            rsylv_b200_plan_holder& H = ctx_holder(ctx);
+            Q.sys_scope = 1;
+            for (int r = 0; r < PL.nranks && (size_t)(5 * r + 4) < H.peer_ptrs.size(); ++r) {
+                if (r == Q.rank) continue;
+                Q.peerY[r] = static_cast<double*>(H.peer_ptrs[5 * r + 0]);
+                Q.peerYexp[r] = static_cast<int*>(H.peer_ptrs[5 * r + 1]);
+                Q.peerYnorm[r] = static_cast<double*>(H.peer_ptrs[5 * r + 2]);
+                Q.peerState[r] = static_cast<int*>(H.peer_ptrs[5 * r + 3]);
+                Q.peerErr[r] = static_cast<int*>(H.peer_ptrs[5 * r + 4]);
+            }
         }
-        ck(ctx, cudaGetLastError(), "wavefront");
-    } else {
-        std::string key = std::to_string(M) + "/" + std::to_string(N) + "/" + std::to_string(TSP);
-        for (int v : rc) key += "," + std::to_string(v);
-        key += "|";
-        for (int v : cc) key += "," + std::to_string(v);
-        if (ctx->tasks_key != key) {
-            std::vector<int>& T = ctx->tasks_host;
-            T.clear();
+    }
+    return Q;
+}
+
+// The tile DAG on every local rank, then the per-rank results: local alpha exponent minimum
+// and max tile norm relative to it (owned tiles only).
+int plan_run(rsylv_b200_ctx* ctx, rsylv_b200_result* res, int* emin_out, double* numax_out) {
+    Plan& PL = ctx_plan(ctx);
+    cudaStream_t st = PL.st;
+    const int M = PL.M, N = PL.N;
+    const size_t ny = PL.ny;
+    ck(ctx, cudaEventRecord(ctx->evp, st), "event");
+    if (PL.nranks == 1) {
+        Problem P = rank_problem(ctx, 0);
+        if (PL.d_probe) P.probe_cap = res->probe_cap;
+        if (PL.scheduler == 1) {
+            res->dag_launches = 0;
             for (int d = 0; d <= M + N - 2; ++d) {
                 const int jlo = std::max(0, d - (M - 1)), jhi = std::min(N - 1, d);
-                for (int j = jlo; j <= jhi; ++j) {
-                    const int i = M - 1 - d + j;
-                    T.push_back(i);
-                    T.push_back(j);
-                }
+                launch_tile_diag(P, d, jhi - jlo + 1, st);
+                res->dag_launches += 1;
             }
-            ctx->tasks_key = key;
-            int* d_tasks = buf<int>(ctx, "tasks", T.size());
-            ck(ctx, cudaMemcpyAsync(d_tasks, T.data(), sizeof(int) * T.size(),
-                                    cudaMemcpyHostToDevice, st), "h2d");
+        } else {
+            launch_persistent(P, ctx->sms, st);
+            res->dag_launches = 1;
         }
-        P.tasks = buf<int>(ctx, "tasks", ctx->tasks_host.size());
-        P.ntasks = (int)(ctx->tasks_host.size() / 2);
+        ck(ctx, cudaGetLastError(), "dag");
+    } else if (PL.local.size() > 1) {
+        std::vector<Problem> probs;
+        for (size_t li = 0; li < PL.local.size(); ++li) probs.push_back(rank_problem(ctx, li));
+        Problem* d_probs = buf<Problem>(ctx, "probs", probs.size());
+        ck(ctx, cudaMemcpyAsync(d_probs, probs.data(), sizeof(Problem) * probs.size(),
+                                cudaMemcpyHostToDevice, st), "h2d");
+        const int R = (int)probs.size();
+        const int grid = std::max(R, ctx->sms / R * R);
+        ck(ctx, launch_persistent_mr(d_probs, R, grid, st), "persistent_mr");
+        res->dag_launches = 1;
+    } else {
+        Problem P = rank_problem(ctx, 0);
         launch_persistent(P, ctx->sms, st);
-        ck(ctx, cudaGetLastError(), "persistent");
+        ck(ctx, cudaGetLastError(), "dag");
         res->dag_launches = 1;
     }
     ck(ctx, cudaEventRecord(ctx->evd, st), "event");
 
-    // ---- alpha reduction (tile_grid.cpp:38-42) in exponent form + joint renormalisation
-    std::vector<int> h_ye(ny);
-    int h_err[4];
-    double h_piv = 0;
-    unsigned long long h_ev[2];
-    ck(ctx, cudaMemcpyAsync(h_ye.data(), yexp, sizeof(int) * ny, cudaMemcpyDeviceToHost, st), "d2h");
-    ck(ctx, cudaMemcpyAsync(h_yn.data(), ynorm, sizeof(double) * ny, cudaMemcpyDeviceToHost, st), "d2h");
-    ck(ctx, cudaMemcpyAsync(h_err, errw, sizeof h_err, cudaMemcpyDeviceToHost, st), "d2h");
-    ck(ctx, cudaMemcpyAsync(&h_piv, pivw, sizeof h_piv, cudaMemcpyDeviceToHost, st), "d2h");
-    ck(ctx, cudaMemcpyAsync(h_ev, evw, sizeof h_ev, cudaMemcpyDeviceToHost, st), "d2h");
-    ck(ctx, cudaStreamSynchronize(st), "solve");
-    res->scaling_events = h_ev[0];
-    if (d_probe) {
-        res->probe_count = (size_t)h_ev[1];
-        const size_t nc = std::min(res->probe_count, res->probe_cap);
-        ck(ctx, cudaMemcpy(res->probe_log, d_probe, nc * sizeof(rsylv_b200_probe_event),
-                           cudaMemcpyDeviceToHost), "d2h");
-    }
-    if (h_err[0] != 0) {
-        res->pivot = h_piv;
-        return h_err[0] == kErrSingular ? RSYLV_SINGULAR : RSYLV_CUDA_ERROR;
-    }
+    // ---- alpha reduction (tile_grid.cpp:38-42) over the owned tiles, exponent form
+    std::vector<int> ye_all(ny, 0);
+    std::vector<double> yn_all(ny, 0.0);
     int emin = 0;
-    for (size_t t = 0; t < ny; ++t) emin = std::min(emin, h_ye[t]);
-    double numax = 0.0;
-    for (size_t t = 0; t < ny; ++t) numax = std::max(numax, std::ldexp(h_yn[t], emin - h_ye[t]));
-    // largest s >= 0 with numax * 2^s <= omega and emin + s <= 0
+    double numax_rel = 0.0;  // max ynorm * 2^(emin - yexp) over owned tiles
+    int first_err = 0;
+    double piv = 0.0;
+    res->scaling_events = 0;
+    for (size_t li = 0; li < PL.local.size(); ++li) {
+        const RankBufs& B = PL.rb[li];
+        std::vector<int> ye(ny);
+        std::vector<double> yn(ny);
+        int h_err[4];
+        double h_piv = 0;
+        unsigned long long h_ev[2];
+        ck(ctx, cudaMemcpyAsync(ye.data(), B.yexp, sizeof(int) * ny, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(ctx, cudaMemcpyAsync(yn.data(), B.ynorm, sizeof(double) * ny, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(ctx, cudaMemcpyAsync(h_err, B.err, sizeof h_err, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(ctx, cudaMemcpyAsync(&h_piv, B.piv, sizeof h_piv, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(ctx, cudaMemcpyAsync(h_ev, B.ev, sizeof h_ev, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(ctx, cudaStreamSynchronize(st), "solve");
+        res->scaling_events += h_ev[0];
+        if (PL.d_probe && li == 0) {
+            res->probe_count = (size_t)h_ev[1];
+            const size_t nc = std::min(res->probe_count, res->probe_cap);
+            ck(ctx, cudaMemcpy(res->probe_log, PL.d_probe, nc * sizeof(rsylv_b200_probe_event),
+                               cudaMemcpyDeviceToHost), "d2h");
+        }
+        if (h_err[0] != 0 && !first_err) {
+            first_err = h_err[0];
+            piv = h_piv;
+        }
+        for (size_t t = 0; t < ny; ++t)
+            if ((int)(t % N) % PL.nranks == PL.local[li]) {
+                ye_all[t] = ye[t];
+                yn_all[t] = yn[t];
+                emin = std::min(emin, ye[t]);
+            }
+    }
+    if (first_err) {
+        res->pivot = piv;
+        return first_err == kErrSingular ? RSYLV_SINGULAR : RSYLV_CUDA_ERROR;
+    }
+    for (size_t li = 0; li < PL.local.size(); ++li)
+        for (size_t t = 0; t < ny; ++t)
+            if ((int)(t % N) % PL.nranks == PL.local[li])
+                numax_rel = std::max(numax_rel, std::ldexp(yn_all[t], emin - ye_all[t]));
+    *emin_out = emin;
+    *numax_out = numax_rel;
+    return RSYLV_OK;
+}
+
+// Largest s >= 0 with numax * 2^s <= omega and emin + s <= 0 (joint renormalisation).
+int alpha_exponent(int emin, double numax, double omega) {
     int s = -emin;
     if (numax > 0.0) {
         int en = 0, eo = 0;
@@ -314,13 +468,21 @@ int solve_device_impl(rsylv_b200_ctx* ctx, const SolveArgs& A) {
         const int smax = eo - en - (mn <= mo ? 0 : 1);
         s = std::max(0, std::min(s, smax));
     }
-    const int alpha_exp = emin + s;
+    return emin + s;
+}
+
+// Consistency scaling fused with the copy-out of the owned columns (tile_grid.cpp:44-52).
+int plan_finish(rsylv_b200_ctx* ctx, int alpha_exp, double numax, int emin, double* y, size_t ldy,
+                rsylv_b200_result* res) {
+    Plan& PL = ctx_plan(ctx);
+    cudaStream_t st = PL.st;
     res->alpha_exp = alpha_exp;
     res->alpha = alpha_exp >= -1022 ? std::ldexp(1.0, alpha_exp) : 0.0;
-    res->max_tile_norm = std::ldexp(numax, s);
-
-    // ---- consistency scaling fused with the copy-out (tile_grid.cpp:44-52)
-    launch_unpack(P, alpha_exp, A.y, (long long)A.ldy, st);
+    res->max_tile_norm = std::ldexp(numax, alpha_exp - emin);
+    for (size_t li = 0; li < PL.local.size(); ++li) {
+        Problem Q = rank_problem(ctx, li);
+        launch_unpack(Q, alpha_exp, y, (long long)ldy, st);
+    }
     ck(ctx, cudaGetLastError(), "unpack");
     ck(ctx, cudaEventRecord(ctx->ev1, st), "event");
     ck(ctx, cudaEventSynchronize(ctx->ev1), "sync");
@@ -334,6 +496,30 @@ int solve_device_impl(rsylv_b200_ctx* ctx, const SolveArgs& A) {
     cudaEventElapsedTime(&ms, ctx->evd, ctx->ev1);
     res->unpack_ms = ms;
     return alpha_exp >= -1022 ? RSYLV_OK : RSYLV_SCALE_UNDERFLOW;
+}
+
+int solve_device_impl(rsylv_b200_ctx* ctx, const SolveArgs& A) {
+    rsylv_b200_result* res = A.res;
+    if (A.opt.tile_size < 2) {  // partition.cpp:75-76
+        res->invalid_reason = RSYLV_REASON_TILE_SIZE;
+        return RSYLV_INVALID_ARGUMENT;
+    }
+    if (A.m == 0 || A.n == 0) {
+        res->alpha = 1.0;
+        res->alpha_exp = 0;
+        return RSYLV_OK;
+    }
+    const int R = std::max(1, std::min(A.opt.virtual_ranks, kMaxRanks));
+    std::vector<int> local;
+    for (int r = 0; r < R; ++r) local.push_back(r);
+    int st = plan_prepare(ctx, A, R, local);
+    if (st != RSYLV_OK) return st;
+    int emin = 0;
+    double numax = 0.0;
+    st = plan_run(ctx, res, &emin, &numax);
+    if (st != RSYLV_OK) return st;
+    const int ae = alpha_exponent(emin, numax, ctx_plan(ctx).omega);
+    return plan_finish(ctx, ae, numax, emin, A.y, A.ldy, res);
 }
 
 int guarded_call(rsylv_b200_ctx* ctx, int (*fn)(rsylv_b200_ctx*, const SolveArgs&),
@@ -392,6 +578,10 @@ void rsylv_b200_destroy(rsylv_b200_ctx* ctx) {
         if (kv.second.p) cudaFree(kv.second.p);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->holder) {
+        close_peers(ctx);
+        delete ctx->holder;
+    }
     if (ctx->evp) cudaEventDestroy(ctx->evp);
     if (ctx->evd) cudaEventDestroy(ctx->evd);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
@@ -463,6 +653,98 @@ int rsylv_b200_solve(rsylv_b200_ctx* ctx, size_t m, size_t n, const double* a, s
     }
     SolveArgs A{m, n, a, b, c, lda, ldb, ldc, ablk, bblk, y, ldy, *opt, ctx->own_stream, res};
     return guarded_call(ctx, solve_host_impl, A);
+}
+
+int rsylv_b200_dist_prepare(rsylv_b200_ctx* ctx, int nranks, int rank, size_t m, size_t n,
+                            const double* a, size_t lda, const unsigned char* ablk,
+                            const double* b, size_t ldb, const unsigned char* bblk,
+                            const double* c, size_t ldc, const rsylv_b200_options* opt,
+                            void* stream, void* handle_out, rsylv_b200_result* res) {
+    if (!ctx || !opt || !res || nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks)
+        return RSYLV_INVALID_ARGUMENT;
+    init_result(res);
+    if (opt->tile_size < 2) {
+        res->invalid_reason = RSYLV_REASON_TILE_SIZE;
+        return RSYLV_INVALID_ARGUMENT;
+    }
+    if (m == 0 || n == 0) return RSYLV_INVALID_ARGUMENT;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return RSYLV_CUDA_ERROR;
+    try {
+        SolveArgs A{m, n, a, b, c, lda, ldb, ldc, ablk, bblk, nullptr, 0, *opt,
+                    stream ? (cudaStream_t)stream : ctx->own_stream, res};
+        A.opt.scheduler = 0;
+        const int st = plan_prepare(ctx, A, nranks, std::vector<int>{rank});
+        if (st != RSYLV_OK) return st;
+        const RankBufs& B = ctx_plan(ctx).rb[0];
+        void* ptrs[5] = {B.Yp, B.yexp, B.ynorm, B.state, B.err};
+        unsigned char* out = static_cast<unsigned char*>(handle_out);
+        for (int k = 0; k < 5; ++k) {
+            cudaIpcMemHandle_t h;
+            ck(ctx, cudaIpcGetMemHandle(&h, ptrs[k]), "ipc handle");
+            std::memcpy(out + 64 * k, &h, 64);
+        }
+        return RSYLV_OK;
+    } catch (const Fail& f) {
+        return f.status;
+    }
+}
+
+int rsylv_b200_dist_run(rsylv_b200_ctx* ctx, const void* all_handles, void* stream,
+                        rsylv_b200_result* res) {
+    if (!ctx || !res) return RSYLV_INVALID_ARGUMENT;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return RSYLV_CUDA_ERROR;
+    try {
+        Plan& PL = ctx_plan(ctx);
+        if (stream) PL.st = (cudaStream_t)stream;
+        rsylv_b200_plan_holder& H = ctx_holder(ctx);
+        const unsigned char* in = static_cast<const unsigned char*>(all_handles);
+        const int R = PL.nranks, me = PL.local[0];
+        if ((int)H.peer_handles.size() != R) {
+            close_peers(ctx);
+            H.peer_handles.assign(R, {});
+            H.peer_ptrs.assign(5 * R, nullptr);
+        }
+        for (int r = 0; r < R; ++r) {
+            if (r == me) continue;
+            std::vector<unsigned char> hb(in + RSYLV_DIST_HANDLE_BYTES * r,
+                                          in + RSYLV_DIST_HANDLE_BYTES * (r + 1));
+            if (H.peer_handles[r] == hb) continue;
+            for (int k = 0; k < 5; ++k)
+                if (H.peer_ptrs[5 * r + k]) cudaIpcCloseMemHandle(H.peer_ptrs[5 * r + k]);
+            for (int k = 0; k < 5; ++k) {
+                cudaIpcMemHandle_t h;
+                std::memcpy(&h, hb.data() + 64 * k, 64);
+                void* p = nullptr;
+                ck(ctx, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "ipc open");
+                H.peer_ptrs[5 * r + k] = p;
+            }
+            H.peer_handles[r] = hb;
+        }
+        int emin = 0;
+        double numax = 0.0;
+        const int st = plan_run(ctx, res, &emin, &numax);
+        res->alpha_exp = emin;
+        res->max_tile_norm = numax;
+        return st;
+    } catch (const Fail& f) {
+        return f.status;
+    }
+}
+
+int rsylv_b200_dist_finish(rsylv_b200_ctx* ctx, int alpha_exp, double* y, size_t ldy,
+                           void* stream, rsylv_b200_result* res) {
+    if (!ctx || !res) return RSYLV_INVALID_ARGUMENT;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return RSYLV_CUDA_ERROR;
+    try {
+        Plan& PL = ctx_plan(ctx);
+        if (stream) PL.st = (cudaStream_t)stream;
+        // res->alpha_exp / max_tile_norm on entry: the global emin and numax (relative to emin)
+        const int emin = res->alpha_exp;
+        const double numax = res->max_tile_norm;
+        return plan_finish(ctx, alpha_exp, numax, emin, y, ldy, res);
+    } catch (const Fail& f) {
+        return f.status;
+    }
 }
 
 int rsylv_b200_robust_update(rsylv_b200_ctx* ctx, size_t m, size_t k, size_t n, double* c,
@@ -581,6 +863,11 @@ int rsylv_b200_robust_update(rsylv_b200_ctx* ctx, size_t m, size_t k, size_t n, 
 int rsylv_b200_debug_counters(unsigned long long* out16, int reset) {
     if (reset) return reset_prof() == cudaSuccess ? RSYLV_OK : RSYLV_CUDA_ERROR;
     return read_prof(out16) == cudaSuccess ? RSYLV_OK : RSYLV_CUDA_ERROR;
+}
+
+// development: average cycles of one warp-level 16x16 sub-block solve (mixed: 2x2 blocks)
+int rsylv_b200_debug_subsolve(int reps, int mixed, long long* cycles) {
+    return bench_subsolve(reps, mixed, cycles) == 0 ? RSYLV_OK : RSYLV_CUDA_ERROR;
 }
 
 int rsylv_b200_generate_quasi_triangular(size_t n, double* dev, size_t ld,
