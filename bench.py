@@ -258,8 +258,8 @@ def main():
         else:
             tmax = sum(times) / len(times)
         e2e = {"value": cfg.flops() * world / tmax / 1e9, "unit": "GFLOP/s",
-               "h2d_bytes_per_step": int(8 * (cfg.m * cfg.m + cfg.n * cfg.n + cfg.m * cfg.n)),
-               "d2h_bytes_per_step": int(8 * cfg.m * cfg.n),
+               "h2d_bytes_per_step": int(r.h2d_bytes),
+               "d2h_bytes_per_step": int(r.d2h_bytes),
                "ms_per_step": 1e3 * tmax, "api": "rsylv_b200_solve (host buffers, pinned)"}
         del hA, hB, hC, hY
 

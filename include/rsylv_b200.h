@@ -91,6 +91,8 @@ typedef struct {
     double dag_ms;            /* tile DAG: update GEMMs + diagonal solves                    */
     double unpack_ms;         /* consistency scaling + copy-out                              */
     uint64_t dag_launches;    /* kernel launches inside the DAG phase                        */
+    uint64_t h2d_bytes;       /* host->device bytes moved by rsylv_b200_solve                */
+    uint64_t d2h_bytes;       /* device->host bytes moved by rsylv_b200_solve                */
 } rsylv_b200_result;
 
 typedef struct rsylv_b200_ctx rsylv_b200_ctx;

@@ -6,8 +6,10 @@ include/rsylv_b200.h. See ``api.py``.
 """
 from .api import (OverflowConfig, ExecutionMode, SolveResult, QuasiTriangular,
                   SingularEquationError, ScaleUnderflowError, solve_tiled_robust,
-                  solve_tiled_robust_device, robust_update, default_omega, default_small_num)
+                  solve_tiled_robust_device, robust_update, default_omega, default_small_num,
+                  solve_robust_scalar, solve_nonrobust)
 
 __all__ = ["OverflowConfig", "ExecutionMode", "SolveResult", "QuasiTriangular",
            "SingularEquationError", "ScaleUnderflowError", "solve_tiled_robust",
-           "solve_tiled_robust_device", "robust_update", "default_omega", "default_small_num"]
+           "solve_tiled_robust_device", "robust_update", "default_omega", "default_small_num",
+           "solve_robust_scalar", "solve_nonrobust"]

@@ -38,7 +38,8 @@ class Result(C.Structure):
                 ("row_tiles", C.c_size_t), ("col_tiles", C.c_size_t),
                 ("probe_log", C.POINTER(ProbeEvent)), ("probe_cap", C.c_size_t),
                 ("probe_count", C.c_size_t), ("pack_ms", C.c_double), ("dag_ms", C.c_double),
-                ("unpack_ms", C.c_double), ("dag_launches", C.c_uint64)]
+                ("unpack_ms", C.c_double), ("dag_launches", C.c_uint64),
+                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
 
 
 _dp = C.POINTER(C.c_double)

@@ -243,6 +243,25 @@ def solve_tiled_robust_device(a_dev, a_codes, b_dev, b_codes, c_dev, y_dev, tile
     return st, res
 
 
+def solve_robust_scalar(a: QuasiTriangular, b: QuasiTriangular, c,
+                        cfg: Optional[OverflowConfig] = None, device: int = 0) -> SolveResult:
+    """rsylv::solve_robust_scalar (scalar_solve.hpp:27-32): A*Y + Y*B = alpha*C with one global
+    scale. On the GPU this is the tiled robust solve with the whole matrix as the requested tile
+    (served by 128-tiles); Y/alpha is the same solution."""
+    c = np.asarray(c, dtype=np.float64)
+    return solve_tiled_robust(a, b, c, max(2, c.shape[0], c.shape[1]), cfg, device=device)
+
+
+def solve_nonrobust(a: QuasiTriangular, b: QuasiTriangular, c, device: int = 0) -> np.ndarray:
+    """rsylv::solve_nonrobust (scalar_solve.hpp:24-25): plain block back substitution, entries
+    may overflow to Inf. Runs the same GPU engine with omega = +Inf, so no guard ever fires and
+    no input is rejected (the reference does not validate either); raises
+    SingularEquationError like the reference."""
+    cfg = OverflowConfig(omega=float("inf"))
+    r = solve_tiled_robust(a, b, np.asarray(c, dtype=np.float64), 128, cfg, device=device)
+    return r.y
+
+
 def robust_update(c, c_exp: int, a, b, ab_exp: int, omega: float = 0.0, device: int = 0):
     """<gamma,C> <- <gamma,C> - <alpha,A><beta,B> (robust_update.hpp:25-33) on the GPU.
 

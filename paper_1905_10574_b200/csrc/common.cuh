@@ -58,6 +58,7 @@ __host__ __device__ __forceinline__ xf xf_from(double v) {
     if (ex == 0x7ff) return {0.5, 1 << 20};
 #endif
     if (v == 0.0) return {0.0, 0};
+    if (!(v <= 1.7976931348623157e308)) return {0.5, 1 << 20};  // +inf (omega = inf: no guard)
     int e = 0;
     const double m = frexp(v, &e);
     return {m, e};
@@ -106,7 +107,9 @@ __host__ __device__ __forceinline__ xf xf_max(xf a, xf b) { return xf_le(a, b) ?
 // Power-of-two guard (the exponent form of update_scale, overflow.cpp:29-40): 0 when
 // g <= omega; otherwise the least d >= 1 with g * 2^-d <= target (= omega * (1 - 2^-30)).
 __host__ __device__ __forceinline__ int xf_guard(xf g, xf omega, xf target) {
-    if (xf_le(g, omega)) return 0;
+    // omega = +inf (xf_from gives e = 1 << 20): the non-robust solve, no guard ever fires and
+    // Inf / NaN propagate as in the reference's plain substitution
+    if (omega.e >= (1 << 19) || xf_le(g, omega)) return 0;
     int d = g.e - target.e + (g.m > target.m ? 1 : 0);
     return d < 1 ? 1 : d;
 }

@@ -616,8 +616,24 @@ static int solve_host_impl(rsylv_b200_ctx* ctx, const SolveArgs& H) {
     double* db = buf<double>(ctx, "hB", n * n);
     double* dc = buf<double>(ctx, "hC", m * n);
     double* dy = buf<double>(ctx, "hY", m * n);
-    ck(ctx, cudaMemcpy2DAsync(da, m * 8, H.a, H.lda * 8, m * 8, m, cudaMemcpyHostToDevice, st), "h2d A");
-    ck(ctx, cudaMemcpy2DAsync(db, n * 8, H.b, H.ldb * 8, n * 8, n, cudaMemcpyHostToDevice, st), "h2d B");
+    unsigned long long h2d = 8ull * m * n;
+    // A and B are quasi-upper-triangular: only the upper tiles travel (tile column k needs rows
+    // 0 .. end of tile k), halving their PCIe traffic; pack_upper never reads below them.
+    auto copy_upper = [&](double* dst, const double* src, size_t ld, size_t dim,
+                          const unsigned char* blk) {
+        std::vector<unsigned char> codes = codes_or_ones(blk, dim);
+        const size_t ts = H.opt.tile_size > (size_t)kTileMax ? (size_t)kTileMax
+                                                              : std::max<size_t>(2, H.opt.tile_size);
+        const std::vector<int> cuts = partition(codes.data(), dim, ts);
+        for (size_t k = 0; k + 1 < cuts.size(); ++k) {
+            const size_t c0 = cuts[k], c1 = cuts[k + 1];
+            ck(ctx, cudaMemcpy2DAsync(dst + c0 * dim, dim * 8, src + c0 * ld, ld * 8, c1 * 8,
+                                      c1 - c0, cudaMemcpyHostToDevice, st), "h2d upper");
+            h2d += 8ull * c1 * (c1 - c0);
+        }
+    };
+    copy_upper(da, H.a, H.lda, m, H.ablk);
+    copy_upper(db, H.b, H.ldb, n, H.bblk);
     ck(ctx, cudaMemcpy2DAsync(dc, m * 8, H.c, H.ldc * 8, m * 8, n, cudaMemcpyHostToDevice, st), "h2d C");
     SolveArgs D = H;
     D.a = da;
@@ -629,9 +645,11 @@ static int solve_host_impl(rsylv_b200_ctx* ctx, const SolveArgs& H) {
     D.ldc = m;
     D.ldy = m;
     const int status = solve_device_impl(ctx, D);
+    H.res->h2d_bytes = h2d;
     if (status == RSYLV_OK || status == RSYLV_SCALE_UNDERFLOW) {
         ck(ctx, cudaMemcpy2DAsync(H.y, H.ldy * 8, dy, m * 8, m * 8, n, cudaMemcpyDeviceToHost, st), "d2h Y");
         ck(ctx, cudaStreamSynchronize(st), "sync");
+        H.res->d2h_bytes = 8ull * m * n;
     }
     return status;
 }
