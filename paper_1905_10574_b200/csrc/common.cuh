@@ -104,6 +104,109 @@ __host__ __device__ __forceinline__ bool xf_le(xf a, xf b) {
 
 __host__ __device__ __forceinline__ xf xf_max(xf a, xf b) { return xf_le(a, b) ? b : a; }
 
+// Integer upper bounds for the update-phase source headers: value <= m * 2^(e - 32) with
+// m in [2^31, 2^32) (or m = 0 for zero), the same exponent convention as xf. Everything here
+// is integer arithmetic: the scalar FP64 pipe shares its datapath with DMMA, so FP64 bound
+// arithmetic in the middle of the update GEMM stalls behind the tensor work. Bounds round UP
+// (xq_from, xq_mul, xq_add); the comparison limits omega / target round DOWN (xq_from_down),
+// so a guard never fires later than the exact rule (at most one binade earlier, and only
+// within 2^-31 of the limit, far inside the 2^-30 shave headroom of overflow.cpp:17).
+#ifdef __CUDACC__
+struct xq {
+    unsigned int m;
+    int e;
+};
+
+__device__ __forceinline__ xq xq_norm64(unsigned long long p, int e) {
+    // p in [2^63, 2^64): m = ceil(p / 2^32)
+    unsigned long long m = (p >> 32) + ((p & 0xffffffffull) != 0 ? 1 : 0);
+    if (m >> 32) {
+        m >>= 1;
+        ++e;
+    }
+    return {(unsigned int)m, e};
+}
+
+__device__ __forceinline__ xq xq_from_bits(double v, bool up) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffull;
+    const int ex = (int)(b >> 52);
+    if (ex == 0x7ff) return {0x80000000u, 1 << 20};  // +inf: above every double (no guard)
+    if (b == 0) return {0u, 0};
+    unsigned long long f = b & 0x000fffffffffffffull;
+    int e;
+    if (ex != 0) {
+        f |= 1ull << 52;  // value = f * 2^(ex - 1075)
+        e = ex - 1022;
+    } else {              // subnormal: value = f * 2^-1074
+        const int lz = __clzll(f) - 11;  // shift the leading one to bit 52
+        f <<= lz;
+        e = 1 - 1022 - lz;
+    }
+    // f in [2^52, 2^53): value = (f / 2^53) * 2^e
+    const unsigned long long p = f << 11;  // [2^63, 2^64)
+    if (up) return xq_norm64(p, e);
+    return {(unsigned int)(p >> 32), e};
+}
+__device__ __forceinline__ xq xq_from(double v) { return xq_from_bits(v, true); }
+__device__ __forceinline__ xq xq_from_down(double v) { return xq_from_bits(v, false); }
+
+__device__ __forceinline__ xq xq_shift(xq a, int k) { return a.m ? xq{a.m, a.e + k} : a; }
+
+__device__ __forceinline__ xq xq_mul(xq a, xq b) {
+    if (a.m == 0 || b.m == 0) return {0u, 0};
+    unsigned long long p = (unsigned long long)a.m * b.m;  // [2^62, 2^64)
+    int e = a.e + b.e;
+    if (!(p >> 63)) {
+        p <<= 1;
+        --e;
+    }
+    return xq_norm64(p, e);
+}
+
+__device__ __forceinline__ xq xq_add(xq a, xq b) {
+    if (a.m == 0) return b;
+    if (b.m == 0) return a;
+    if (a.e < b.e) {
+        const xq t = a;
+        a = b;
+        b = t;
+    }
+    const int d = a.e - b.e;
+    // b < 2^(b.e) <= 2^(a.e - d): below one unit of a's last place when d >= 32
+    const unsigned long long bs = d >= 32 ? 1ull : ((unsigned long long)b.m >> d) + ((b.m & ((1u << d) - 1u)) != 0 ? 1 : 0);
+    unsigned long long s = (unsigned long long)a.m + bs;
+    int e = a.e;
+    if (s >> 32) {
+        s = (s >> 1) + (s & 1);
+        ++e;
+        if (s >> 32) {
+            s >>= 1;
+            ++e;
+        }
+    }
+    return {(unsigned int)s, e};
+}
+
+__device__ __forceinline__ bool xq_le(xq a, xq b) {
+    if (a.m == 0) return true;
+    if (b.m == 0) return false;
+    if (a.e != b.e) return a.e < b.e;
+    return a.m <= b.m;
+}
+
+// xf_guard on integer bounds (omega / target from xq_from_down)
+__device__ __forceinline__ int xq_guard(xq g, xq omega, xq target) {
+    if (omega.e >= (1 << 19) || xq_le(g, omega)) return 0;
+    const int d = g.e - target.e + (g.m > target.m ? 1 : 0);
+    return d < 1 ? 1 : d;
+}
+
+__device__ __forceinline__ xf xq_to_xf(xq a) {
+    if (a.m == 0) return xf_zero();
+    return {(double)a.m * 0x1p-32, a.e};  // exact; (m / 2^32) in [0.5, 1)
+}
+#endif  // __CUDACC__
+
 // Power-of-two guard (the exponent form of update_scale, overflow.cpp:29-40): 0 when
 // g <= omega; otherwise the least d >= 1 with g * 2^-d <= target (= omega * (1 - 2^-30)).
 __host__ __device__ __forceinline__ int xf_guard(xf g, xf omega, xf target) {

@@ -19,6 +19,7 @@ void launch_pack_full(const double* src, long long ld, const Problem& P, double*
                       cudaStream_t st);
 void launch_tile_diag(const Problem& P, int d, int ntiles, cudaStream_t st);
 void launch_update_only(const Problem& P, int i, int j, cudaStream_t st);
+void launch_update_bench(const Problem& P, int ctas, cudaStream_t st);
 void launch_persistent(const Problem& P, int grid, cudaStream_t st);
 cudaError_t launch_persistent_mr(const Problem* probs_dev, int nranks_here, int grid,
                                  cudaStream_t st);

@@ -377,7 +377,10 @@ int plan_run(rsylv_b200_ctx* ctx, rsylv_b200_result* res, int* emin_out, double*
     if (PL.nranks == 1) {
         Problem P = rank_problem(ctx, 0);
         if (PL.d_probe) P.probe_cap = res->probe_cap;
-        if (PL.scheduler == 1) {
+        if (PL.scheduler == 2) {  // development: update-phase throughput (garbage results)
+            launch_update_bench(P, ctx->sms, st);
+            res->dag_launches = 1;
+        } else if (PL.scheduler == 1) {
             res->dag_launches = 0;
             for (int d = 0; d <= M + N - 2; ++d) {
                 const int jlo = std::max(0, d - (M - 1)), jhi = std::min(N - 1, d);

@@ -18,7 +18,6 @@ for name in sys.argv[1:] or ["c1"]:
     ntiles = res.row_tiles * res.col_tiles
     names = ["update", "setup", "subsolve", "in-tile upd", "finalize"]
     tot = sum(out[i] for i in range(5))
-    print("   subsolve detail (per warp, us per tile): setup=%.1f rhs=%.1f solve+vote=%.1f install+colupd=%.1f" % tuple(out[i] / ntiles / 1965 for i in (5, 6, 7, 8)))
-    print("   flag-wait=%.1f us/tile, chunks=%d prescaled=%d (%.1f%%)" % (out[9] / ntiles / 1965, out[10], out[11], 100.0 * out[11] / max(1, out[10])))
+    print("   flag-wait=%.1f us/tile, metadata-arrival=%.1f us/tile, header=%.1f us/tile, chunks=%d prescaled=%d (%.1f%%)" % (out[9] / ntiles / 1965, out[14] / ntiles / 1965, out[13] / ntiles / 1965, out[10], out[11], 100.0 * out[11] / max(1, out[10])))
     print(name, "dag_ms", round(res.dag_ms, 2), "tiles", ntiles, " ".join(
         f"{names[i]}={out[i] / ntiles / 1965:.1f}us({100 * out[i] / tot:.0f}%)" for i in range(5)))
