@@ -249,6 +249,8 @@ struct Problem {
     double* Ypack;              // all tiles of Y, slot i*N + j
     double* anorm;              // M*M, (i,k) at i*M+k (upper)
     double* bnorm;              // N*N, (l,j) at l*N+j (upper)
+    int* aexp;                  // M*M: off-diagonal A tiles are stored as A_ik * 2^-aexp (pack)
+    int* bexp;                  // N*N: the same for B
     double* ynorm;              // M*N current cached tile norm
     int* yexp;                  // M*N tile exponent (scale = 2^yexp, yexp <= 0)
     int* uexp;                  // M*N exponent after the update phase

@@ -14,7 +14,7 @@ cudaError_t reset_prof();
 cudaError_t configure_kernels();
 
 void launch_pack_upper(const double* src, long long ld, const int* cut, int T, int TSP,
-                       double* dst, double* norms, cudaStream_t st);
+                       double* dst, double* norms, int* sexp, cudaStream_t st);
 void launch_pack_full(const double* src, long long ld, const Problem& P, double* norms,
                       cudaStream_t st);
 void launch_tile_diag(const Problem& P, int d, int ntiles, cudaStream_t st);

@@ -214,6 +214,8 @@ int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std:
     double* Bp = buf<double>(ctx, "Bpack", nb * slot + slack);
     double* anorm = buf<double>(ctx, "anorm", (size_t)M * M);
     double* bnorm = buf<double>(ctx, "bnorm", (size_t)N * N);
+    int* aexp = buf<int>(ctx, "aexp", (size_t)M * M);
+    int* bexp = buf<int>(ctx, "bexp", (size_t)N * N);
     ck(ctx, cudaMemcpyAsync(d_rc, rc.data(), sizeof(int) * (M + 1), cudaMemcpyHostToDevice, st), "h2d");
     ck(ctx, cudaMemcpyAsync(d_cc, cc.data(), sizeof(int) * (N + 1), cudaMemcpyHostToDevice, st), "h2d");
     ck(ctx, cudaMemcpyAsync(d_ab, ac.data(), m, cudaMemcpyHostToDevice, st), "h2d");
@@ -228,6 +230,8 @@ int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std:
     P.Bpack = Bp;
     P.anorm = anorm;
     P.bnorm = bnorm;
+    P.aexp = aexp;
+    P.bexp = bexp;
     P.nsub_r = P.nsub_c = TSP / kBM;
     P.omega = PL.omega;
     P.small_num = PL.small_num;
@@ -235,8 +239,8 @@ int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std:
     P.x_target = host_xf(PL.omega * (1.0 - 0x1p-30));
     P.nranks = nranks;
 
-    launch_pack_upper(A.a, (long long)A.lda, d_rc, M, TSP, Ap, anorm, st);
-    launch_pack_upper(A.b, (long long)A.ldb, d_cc, N, TSP, Bp, bnorm, st);
+    launch_pack_upper(A.a, (long long)A.lda, d_rc, M, TSP, Ap, anorm, aexp, st);
+    launch_pack_upper(A.b, (long long)A.ldb, d_cc, N, TSP, Bp, bnorm, bexp, st);
 
     PL.rb.assign(local.size(), RankBufs{});
     PL.d_probe = nullptr;
@@ -802,6 +806,8 @@ int rsylv_b200_robust_update(rsylv_b200_ctx* ctx, size_t m, size_t k, size_t n, 
         double* Yp = buf<double>(ctx, "ruYpack", 2 * slot + slack);
         double* an = buf<double>(ctx, "ruan", 4);
         double* bn = buf<double>(ctx, "rubn", 1);
+        int* ax = buf<int>(ctx, "ruax", 4);
+        int* bx = buf<int>(ctx, "rubx", 1);
         double* yn = buf<double>(ctx, "ruyn", 2);
         int* ye = buf<int>(ctx, "ruye", 2);
         int* ue = buf<int>(ctx, "ruue", 2);
@@ -835,6 +841,8 @@ int rsylv_b200_robust_update(rsylv_b200_ctx* ctx, size_t m, size_t k, size_t n, 
         P.Ypack = Yp;
         P.anorm = an;
         P.bnorm = bn;
+        P.aexp = ax;
+        P.bexp = bx;
         P.ynorm = yn;
         P.yexp = ye;
         P.uexp = ue;
@@ -849,7 +857,8 @@ int rsylv_b200_robust_update(rsylv_b200_ctx* ctx, size_t m, size_t k, size_t n, 
         P.small_num = DBL_MIN / DBL_EPSILON;
         P.x_omega = host_xf(P.omega);
         P.x_target = host_xf(P.omega * (1.0 - 0x1p-30));
-        launch_pack_upper(dA, (long long)mk, d_rc, M, TSP, Ap, an, st);
+        launch_pack_upper(dA, (long long)mk, d_rc, M, TSP, Ap, an, ax, st);
+        ck(ctx, cudaMemsetAsync(bx, 0, sizeof(int), st), "memset");
         launch_pack_full(dY, (long long)mk, P, yn, st);
         const int exps[2] = {c_exp ? *c_exp : 0, ab_exp};
         ck(ctx, cudaMemcpyAsync(ye, exps, 8, cudaMemcpyHostToDevice, st), "h2d");
