@@ -269,6 +269,22 @@ def main():
         cpu = {"value": scfg.flops() / times[0] / 1e9, "unit": "GFLOP/s", "cores": cores,
                "kind": "reference", "sample": sample}
 
+    # DRAM traffic of the dominant kernel per launch, from the committed ncu capture of the same
+    # command (ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum -k k_persistent)
+    traffic, traffic_src = None, None
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01",
+                         f"traffic_{cfg.name}_k_persistent.csv")
+    if os.path.exists(tpath) and args.scheduler == 0 and world == 1:
+        import csv
+        vals = {}
+        with open(tpath) as fh:
+            for r in csv.reader(l for l in fh if not l.startswith("==")):
+                if len(r) > 14 and r[12].startswith("dram__bytes"):
+                    vals[r[12]] = float(r[14].replace(",", ""))
+        if len(vals) == 2:
+            traffic = vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
+            traffic_src = os.path.relpath(tpath, os.path.dirname(os.path.abspath(__file__)))
+
     dag = sum(dag_ms) / len(dag_ms)
     achieved = cfg.flops() / (dag / 1e3) / 1e12
     if rank == 0:
@@ -288,7 +304,10 @@ def main():
                        "scaling_events": int(res.scaling_events)},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": achieved / FP64_DMMA_PEAK_TFLOPS,
-                         "traffic": None, "kernel": "k_persistent (tile DAG)",
+                         "traffic": traffic, "traffic_unit": "bytes per launch (DRAM read+write)",
+                         "traffic_source": traffic_src,
+                         "algorithmic_bytes": cfg.alg_bytes() if hasattr(cfg, "alg_bytes") else None,
+                         "kernel": "k_persistent (tile DAG)",
                          "peak_source": "measured FP64 DMMA microbenchmark (profiles/"
                                         "r01_fp64_peak_probe.log); cuBLAS DGEMM 35.46"},
             "clocks": clk.summary(),

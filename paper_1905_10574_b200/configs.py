@@ -45,6 +45,10 @@ class Config:
     def flops(self) -> float:
         return float(self.m) * self.n * (self.m + self.n)
 
+    def alg_bytes(self) -> float:
+        """read the upper A and B, read C, write Y (8-byte doubles)."""
+        return 8.0 * (self.m * self.m / 2 + self.n * self.n / 2 + 2.0 * self.m * self.n)
+
     def scaled(self, m: int, n: int | None = None, tile: int | None = None) -> "Config":
         d = dict(self.__dict__)
         d.update(m=m, n=n if n is not None else m, tile=tile or self.tile,
