@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "rsylv/errors.hpp"
+#include "rsylv/matrix_io.hpp"
 #include "rsylv/overflow.hpp"
 #include "rsylv/robust_update.hpp"
 #include "rsylv/scalar_solve.hpp"
@@ -216,6 +217,15 @@ int ref_dense_kron_solve(std::size_t m, std::size_t n, const double* a, const un
         DenseMatrix r = dense_kron_solve(qa, qb, ConstMatrixView{c, m, n, m});
         from_dense(r, y, m);
     }, nullptr);
+}
+
+// matrix_io.hpp format_double (std::to_chars shortest round trip): the CSV / matrix-file number
+// format, for pinning paper_1905_10574_b200/records.py. Returns the string length.
+int ref_format_double(double v, char* buf, std::size_t cap) {
+    const std::string s = format_double(v);
+    if (s.size() + 1 > cap) return -1;
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    return static_cast<int>(s.size());
 }
 
 } // extern "C"
