@@ -896,8 +896,8 @@ int rsylv_b200_debug_counters(unsigned long long* out16, int reset) {
 }
 
 // development: average cycles of one warp-level 16x16 sub-block solve (mixed: 2x2 blocks)
-int rsylv_b200_debug_subsolve(int reps, int mixed, long long* cycles) {
-    return bench_subsolve(reps, mixed, cycles) == 0 ? RSYLV_OK : RSYLV_CUDA_ERROR;
+int rsylv_b200_debug_subsolve(int reps, int mode, long long* cycles, double* out256) {
+    return bench_subsolve(reps, mode, cycles, out256) == 0 ? RSYLV_OK : RSYLV_CUDA_ERROR;
 }
 
 int rsylv_b200_generate_quasi_triangular(size_t n, double* dev, size_t ld,

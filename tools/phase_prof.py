@@ -18,6 +18,9 @@ for name in sys.argv[1:] or ["c1"]:
     ntiles = res.row_tiles * res.col_tiles
     names = ["update", "setup", "subsolve", "in-tile upd", "finalize"]
     tot = sum(out[i] for i in range(5))
+    if out[6]:
+        print("   per sub-block (per warp): solve %.2f us, norm %.2f us, count %d" % (out[5] / out[6] / 1965, out[7] / out[6] / 1965, out[6]))
+    print("   column-path fallbacks to the exact sub-block solver: %d" % out[12])
     print("   flag-wait=%.1f us/tile, metadata-arrival=%.1f us/tile, header=%.1f us/tile, chunks=%d prescaled=%d (%.1f%%)" % (out[9] / ntiles / 1965, out[14] / ntiles / 1965, out[13] / ntiles / 1965, out[10], out[11], 100.0 * out[11] / max(1, out[10])))
     print(name, "dag_ms", round(res.dag_ms, 2), "tiles", ntiles, " ".join(
         f"{names[i]}={out[i] / ntiles / 1965:.1f}us({100 * out[i] / tot:.0f}%)" for i in range(5)))
