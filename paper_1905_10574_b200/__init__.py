@@ -8,8 +8,9 @@ from .api import (OverflowConfig, ExecutionMode, SolveResult, QuasiTriangular,
                   SingularEquationError, ScaleUnderflowError, solve_tiled_robust,
                   solve_tiled_robust_device, robust_update, default_omega, default_small_num,
                   solve_robust_scalar, solve_nonrobust)
+from .bartels_stewart import solve_sylvester
 
 __all__ = ["OverflowConfig", "ExecutionMode", "SolveResult", "QuasiTriangular",
            "SingularEquationError", "ScaleUnderflowError", "solve_tiled_robust",
            "solve_tiled_robust_device", "robust_update", "default_omega", "default_small_num",
-           "solve_robust_scalar", "solve_nonrobust"]
+           "solve_robust_scalar", "solve_nonrobust", "solve_sylvester"]

@@ -175,3 +175,14 @@ def test_cli_without_device_fails_loudly(capsys):
         pytest.skip("device present")
     assert cli.main(["verify", "--sizes", "6", "--count", "1"]) == 2
     assert "no_device" in capsys.readouterr().err
+
+
+def test_bartels_stewart_host_parts():
+    from paper_1905_10574_b200 import bartels_stewart as bs
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((9, 9))
+    t, u = bs.schur_real(a)
+    assert np.allclose(u @ t @ u.T, a, atol=1e-12)
+    assert np.allclose(np.tril(t, -2), 0.0)
+    with pytest.raises(ValueError):
+        bs.solve_sylvester(np.eye(3), np.eye(2), np.ones((3, 3)))
