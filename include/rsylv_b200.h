@@ -61,6 +61,9 @@ typedef struct {
     int virtual_ranks; /* >1: emulate that many GPUs on this device (tile columns block-cyclic,
                           solved tiles pushed between per-rank workspaces) -- validates the
                           multi-GPU exchange on one GPU; 0/1 = off                          */
+    int host_pipeline; /* rsylv_b200_solve only: stream the inputs in (H2D + pack per tile
+                          column) while the solve runs. 0: automatic (from 64 tiles),
+                          1: always, -1: never (copy everything first)                     */
 } rsylv_b200_options;
 
 /* One TileProbe event (tiled_solve.hpp:24-27): tile (k, l) came to rest with local scale

@@ -183,12 +183,14 @@ def solve_tiled_robust(a: QuasiTriangular, b: QuasiTriangular, c, tile_size: int
                        mode: Optional[ExecutionMode] = None,
                        probe: Optional[Callable[[int, int, float, float], None]] = None,
                        scheduler: int = 0, device: int = 0,
-                       probe_capacity: int = 1 << 20, virtual_ranks: int = 1) -> SolveResult:
+                       probe_capacity: int = 1 << 20, virtual_ranks: int = 1,
+                       host_pipeline: int = 0) -> SolveResult:
     """Solves A*Y + Y*B = alpha*C with every tile of Y bounded by cfg.omega (tiled_solve.hpp:29-40).
 
     HOST arrays in, HOST array out (the reference calling convention). ``mode.workers`` is the
     reference's worker count; a single GPU serves every value (multi-GPU runs go through
-    bench.py / torchrun)."""
+    bench.py / torchrun). ``host_pipeline`` (0 auto, 1 on, -1 off) streams the inputs to the
+    device tile column by tile column while the solve runs (rsylv_b200_options)."""
     cfg = cfg or OverflowConfig()
     c = np.asarray(c, dtype=np.float64)
     if c.ndim != 2 or c.shape[0] != a.dim() or c.shape[1] != b.dim():
@@ -196,7 +198,8 @@ def solve_tiled_robust(a: QuasiTriangular, b: QuasiTriangular, c, tile_size: int
     m, n = c.shape
     cf = np.asfortranarray(c)
     y = np.zeros((m, n), order="F")
-    opt = nat.Options(cfg.omega, cfg.small_num, int(tile_size), scheduler, int(virtual_ranks))
+    opt = nat.Options(cfg.omega, cfg.small_num, int(tile_size), scheduler, int(virtual_ranks),
+                      int(host_pipeline))
     res = nat.Result()
     pbuf = None
     if probe is not None:

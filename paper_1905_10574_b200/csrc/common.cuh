@@ -27,7 +27,7 @@ constexpr int kLDA = kBM + 4;    // smem A stage: [kKC][kLDA] (rows contiguous),
 constexpr int kLDB = kKC + 4;    // smem B stage: [kBM][kLDB] (k contiguous), conflict-free
 
 // error codes written to the device error word (first writer wins)
-enum : int { kErrNone = 0, kErrSingular = 2, kErrWatchdog = 8, kErrInternal = 9 };
+enum : int { kErrNone = 0, kErrSingular = 2, kErrWatchdog = 8, kErrInternal = 9, kErrInvalid = 10 };
 constexpr unsigned long long kWatchdogNs = 60ull * 1000000000ull;  // a source tile never arriving
 
 // 2^e as a double for e in [-1022, 1023] (exact, no libm call).
@@ -249,6 +249,8 @@ struct Problem {
     double* Ypack;              // all tiles of Y, slot i*N + j
     double* anorm;              // M*M, (i,k) at i*M+k (upper)
     double* bnorm;              // N*N, (l,j) at l*N+j (upper)
+    int* in_ready;              // host pipeline: packed tile columns of A (from the right), B,
+                                // C (from the left); nullptr when every input is packed upfront
     int* aexp;                  // M*M: off-diagonal A tiles are stored as A_ik * 2^-aexp (pack)
     int* bexp;                  // N*N: the same for B
     double* ynorm;              // M*N current cached tile norm
@@ -259,6 +261,7 @@ struct Problem {
     int* udone;                 // M*N: finished update subtasks
     int* err;                   // first error code
     double* err_pivot;
+    double* tile_pivot;         // M*N: pivot of a tile's singular block (err[1] picks the tile)
     unsigned long long* events; // scaling events
     ProbeEv* probe;             // optional probe log
     unsigned long long* probe_count;

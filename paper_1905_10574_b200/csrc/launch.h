@@ -20,6 +20,12 @@ void launch_pack_full(const double* src, long long ld, const Problem& P, double*
 void launch_tile_diag(const Problem& P, int d, int ntiles, cudaStream_t st);
 void launch_update_only(const Problem& P, int i, int j, cudaStream_t st);
 void launch_update_bench(const Problem& P, int ctas, cudaStream_t st);
+void launch_pack_upper_col(const double* src, long long ld, const int* cut, int T, int TSP,
+                           double* dst, double* norms, int* sexp, int k, cudaStream_t st);
+void launch_pack_full_col(const double* src, long long ld, const Problem& P, double* norms,
+                          int j, cudaStream_t st);
+void launch_set_ready(int* ready, int a, int b, int c, cudaStream_t st);
+void launch_validate_col(const Problem& P, int* reason, int kA, int jB, int jC, cudaStream_t st);
 void launch_persistent(const Problem& P, int grid, cudaStream_t st);
 cudaError_t launch_persistent_mr(const Problem* probs_dev, int nranks_here, int grid,
                                  cudaStream_t st);

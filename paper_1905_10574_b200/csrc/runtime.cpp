@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <string>
 #include <vector>
@@ -34,6 +35,8 @@ struct rsylv_b200_ctx {
     std::string last_error;
     bool configured = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evp = nullptr, evd = nullptr;
+    cudaStream_t side_stream = nullptr;                  // host pipeline: H2D + pack
+    cudaEvent_t ev_side0 = nullptr, ev_side = nullptr;
     struct rsylv_b200_plan_holder* holder = nullptr;
 };
 
@@ -113,6 +116,7 @@ struct RankBufs {
     int* udone = nullptr;
     int* err = nullptr;
     double* piv = nullptr;
+    double* tpiv = nullptr;  // per-tile pivots of singular failures
     unsigned long long* ev = nullptr;
     int* tnext = nullptr;
     int* tasks = nullptr;
@@ -131,6 +135,7 @@ struct Plan {
     cudaStream_t st = nullptr;
     int scheduler = 0;
     rsylv_b200_probe_event* d_probe = nullptr;
+    int* d_reason = nullptr;  // host pipeline: first failing argument check (device)
 };
 
 }  // namespace
@@ -160,7 +165,9 @@ void close_peers(rsylv_b200_ctx* ctx) {
 // Steps shared by every mode: partition (tile cut moved earlier around 2x2 blocks), device
 // workspaces, TileGrid + compute_bounds as one pack pass, validation in the reference order
 // (tile_grid.cpp:59-74, tiled_solve.cpp:74-80), per-rank task lists in anti-diagonal order.
-int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std::vector<int>& local) {
+// deferred: the host pipeline packs (and validates) the inputs itself while the DAG runs
+int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std::vector<int>& local,
+                 bool deferred = false) {
     rsylv_b200_result* res = A.res;
     Plan& PL = ctx_plan(ctx);
     const size_t m = A.m, n = A.n;
@@ -239,8 +246,18 @@ int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std:
     P.x_target = host_xf(PL.omega * (1.0 - 0x1p-30));
     P.nranks = nranks;
 
-    launch_pack_upper(A.a, (long long)A.lda, d_rc, M, TSP, Ap, anorm, aexp, st);
-    launch_pack_upper(A.b, (long long)A.ldb, d_cc, N, TSP, Bp, bnorm, bexp, st);
+    PL.d_reason = nullptr;
+    if (deferred) {
+        int* rdy = buf<int>(ctx, "inready", 4);
+        PL.d_reason = buf<int>(ctx, "reason", 1);
+        const int four = 4;
+        ck(ctx, cudaMemsetAsync(rdy, 0, 4 * sizeof(int), st), "memset");
+        ck(ctx, cudaMemcpyAsync(PL.d_reason, &four, sizeof(int), cudaMemcpyHostToDevice, st), "h2d");
+        P.in_ready = rdy;
+    } else {
+        launch_pack_upper(A.a, (long long)A.lda, d_rc, M, TSP, Ap, anorm, aexp, st);
+        launch_pack_upper(A.b, (long long)A.ldb, d_cc, N, TSP, Bp, bnorm, bexp, st);
+    }
 
     PL.rb.assign(local.size(), RankBufs{});
     PL.d_probe = nullptr;
@@ -257,6 +274,7 @@ int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std:
         B.udone = buf<int>(ctx, ("udone" + sfx).c_str(), ny);
         B.err = buf<int>(ctx, ("err" + sfx).c_str(), 4);
         B.piv = buf<double>(ctx, ("pivot" + sfx).c_str(), 1);
+        B.tpiv = buf<double>(ctx, ("tpivot" + sfx).c_str(), ny);
         B.ev = buf<unsigned long long>(ctx, ("events" + sfx).c_str(), 2);
         B.tnext = buf<int>(ctx, ("tnext" + sfx).c_str(), 1);
         ck(ctx, cudaMemsetAsync(B.Yp + ny * slot, 0, slack * sizeof(double), st), "memset");
@@ -270,7 +288,7 @@ int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std:
         Q.uexp = B.uexp;
         Q.state = B.state;
         Q.udone = B.udone;
-        launch_pack_full(A.c, (long long)A.ldc, Q, B.ynorm, st);
+        if (!deferred) launch_pack_full(A.c, (long long)A.ldc, Q, B.ynorm, st);
         // task list: owned tile columns, anti-diagonal order
         std::vector<int> T;
         for (int d = 0; d <= M + N - 2; ++d) {
@@ -291,6 +309,7 @@ int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std:
         PL.d_probe = buf<rsylv_b200_probe_event>(ctx, "probe", res->probe_cap);
     ck(ctx, cudaGetLastError(), "pack");
 
+    if (deferred) return RSYLV_OK;  // validated on the device after the last pack
     std::vector<double> h_an((size_t)M * M), h_bn((size_t)N * N), h_yn(ny);
     ck(ctx, cudaMemcpyAsync(h_an.data(), anorm, sizeof(double) * M * M, cudaMemcpyDeviceToHost, st), "d2h");
     ck(ctx, cudaMemcpyAsync(h_bn.data(), bnorm, sizeof(double) * N * N, cudaMemcpyDeviceToHost, st), "d2h");
@@ -331,6 +350,7 @@ Problem rank_problem(rsylv_b200_ctx* ctx, size_t li) {
     Q.udone = B.udone;
     Q.err = B.err;
     Q.err_pivot = B.piv;
+    Q.tile_pivot = B.tpiv;
     Q.events = B.ev;
     Q.task_next = B.tnext;
     Q.tasks = B.tasks;
@@ -372,7 +392,12 @@ Problem rank_problem(rsylv_b200_ctx* ctx, size_t li) {
 
 // The tile DAG on every local rank, then the per-rank results: local alpha exponent minimum
 // and max tile norm relative to it (owned tiles only).
-int plan_run(rsylv_b200_ctx* ctx, rsylv_b200_result* res, int* emin_out, double* numax_out) {
+// side: host pipeline -- the DAG starts on all but kPipeReserve SMs, side() enqueues the H2D +
+// pack + validation work (and the remaining DAG CTAs) on the side stream, which the main
+// stream joins before the alpha reduction
+constexpr int kPipeReserve = 4;
+int plan_run(rsylv_b200_ctx* ctx, rsylv_b200_result* res, int* emin_out, double* numax_out,
+             const std::function<void()>* side = nullptr) {
     Plan& PL = ctx_plan(ctx);
     cudaStream_t st = PL.st;
     const int M = PL.M, N = PL.N;
@@ -391,6 +416,13 @@ int plan_run(rsylv_b200_ctx* ctx, rsylv_b200_result* res, int* emin_out, double*
                 launch_tile_diag(P, d, jhi - jlo + 1, st);
                 res->dag_launches += 1;
             }
+        } else if (side) {
+            // the side stream starts after the setup on st, NOT after the DAG launched below
+            ck(ctx, cudaEventRecord(ctx->ev_side0, st), "event");
+            launch_persistent(P, std::max(1, ctx->sms - kPipeReserve), st);
+            (*side)();
+            ck(ctx, cudaStreamWaitEvent(st, ctx->ev_side, 0), "join");
+            res->dag_launches = 2;
         } else {
             launch_persistent(P, ctx->sms, st);
             res->dag_launches = 1;
@@ -421,6 +453,7 @@ int plan_run(rsylv_b200_ctx* ctx, rsylv_b200_result* res, int* emin_out, double*
     double numax_rel = 0.0;  // max ynorm * 2^(emin - yexp) over owned tiles
     int first_err = 0;
     double piv = 0.0;
+    int best_enc = -1;  // singular failures: the earliest tile in the reference order wins
     res->scaling_events = 0;
     for (size_t li = 0; li < PL.local.size(); ++li) {
         const RankBufs& B = PL.rb[li];
@@ -442,8 +475,18 @@ int plan_run(rsylv_b200_ctx* ctx, rsylv_b200_result* res, int* emin_out, double*
             ck(ctx, cudaMemcpy(res->probe_log, PL.d_probe, nc * sizeof(rsylv_b200_probe_event),
                                cudaMemcpyDeviceToHost), "d2h");
         }
-        if (h_err[0] != 0 && !first_err) {
-            first_err = h_err[0];
+        if (h_err[0] == kErrSingular) {
+            if (h_err[1] > best_enc) {  // enc = INT_MAX - priority: larger is earlier
+                best_enc = h_err[1];
+                const int pri = 0x7fffffff - h_err[1];
+                const int k = M - 1 - pri / N, l = pri % N;
+                if ((l % PL.nranks) == PL.local[li])
+                    ck(ctx, cudaMemcpy(&piv, B.tpiv + (size_t)k * N + l, sizeof(double),
+                                       cudaMemcpyDeviceToHost), "d2h");
+            }
+            if (!first_err) first_err = h_err[0];
+        } else if (h_err[0] != 0 && (!first_err || first_err == kErrSingular)) {
+            first_err = h_err[0];  // non-singular errors (watchdog, invalid) dominate
             piv = h_piv;
         }
         for (size_t t = 0; t < ny; ++t)
@@ -455,6 +498,13 @@ int plan_run(rsylv_b200_ctx* ctx, rsylv_b200_result* res, int* emin_out, double*
     }
     if (first_err) {
         res->pivot = piv;
+        if (first_err == kErrInvalid && PL.d_reason) {  // host pipeline: device-side checks
+            int code = 4;
+            ck(ctx, cudaMemcpy(&code, PL.d_reason, sizeof(int), cudaMemcpyDeviceToHost), "d2h");
+            res->invalid_reason = code == 1 ? RSYLV_REASON_A_BOUND
+                                : code == 2 ? RSYLV_REASON_B_BOUND : RSYLV_REASON_C_BOUND;
+            return RSYLV_INVALID_ARGUMENT;
+        }
         return first_err == kErrSingular ? RSYLV_SINGULAR : RSYLV_CUDA_ERROR;
     }
     for (size_t li = 0; li < PL.local.size(); ++li)
@@ -569,6 +619,9 @@ int rsylv_b200_create(int device, rsylv_b200_ctx** out) {
     ctx->device = device;
     cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
     if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_side0, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_side, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
         cudaEventCreate(&ctx->evp) != cudaSuccess || cudaEventCreate(&ctx->evd) != cudaSuccess) {
         delete ctx;
@@ -592,6 +645,9 @@ void rsylv_b200_destroy(rsylv_b200_ctx* ctx) {
     if (ctx->evp) cudaEventDestroy(ctx->evp);
     if (ctx->evd) cudaEventDestroy(ctx->evd);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
+    if (ctx->ev_side0) cudaEventDestroy(ctx->ev_side0);
+    if (ctx->ev_side) cudaEventDestroy(ctx->ev_side);
     delete ctx;
 }
 
@@ -616,6 +672,78 @@ int rsylv_b200_solve_device(rsylv_b200_ctx* ctx, size_t m, size_t n, const doubl
     return guarded_call(ctx, solve_device_impl, A);
 }
 
+// Host pipeline (rsylv_b200_options.host_pipeline): the DAG starts on all but kPipeReserve SMs
+// while a side stream copies the inputs tile column by tile column -- A from the right, B and
+// C from the left, the order in which the anti-diagonal task list consumes them -- packs each
+// column on the reserved SMs, checks its tile norms on the device (the reference's argument
+// checks and reason order; a failure aborts the DAG and returns RSYLV_INVALID_ARGUMENT) and
+// publishes its count (tile tasks wait on these counters at their start); finally it launches
+// the remaining DAG CTAs, which join the task queue. Overlaps the H2D traffic with the solve.
+static int solve_host_pipelined(rsylv_b200_ctx* ctx, const SolveArgs& H, double* da, double* db,
+                                double* dc, double* dy) {
+    cudaStream_t st = H.st;
+    const size_t m = H.m, n = H.n;
+    SolveArgs D = H;
+    D.a = da;
+    D.b = db;
+    D.c = dc;
+    D.y = dy;
+    D.lda = m;
+    D.ldb = n;
+    D.ldc = m;
+    D.ldy = m;
+    int status = plan_prepare(ctx, D, 1, std::vector<int>{0}, true);
+    if (status != RSYLV_OK) return status;
+    Plan& PL = ctx_plan(ctx);
+    const int M = PL.M, N = PL.N, TSP = PL.TSP;
+    const Problem Q = rank_problem(ctx, 0);
+    unsigned long long h2d = 0;
+    std::function<void()> side = [&]() {
+        cudaStream_t ss = ctx->side_stream;
+        ck(ctx, cudaStreamWaitEvent(ss, ctx->ev_side0, 0), "wait");
+        for (int t = 0; t < std::max(M, N); ++t) {
+            if (t < M) {  // A tile column k (its upper part), from the right
+                const int k = M - 1 - t;
+                const size_t c0 = PL.rc[k], c1 = PL.rc[k + 1];
+                ck(ctx, cudaMemcpy2DAsync(da + c0 * m, m * 8, H.a + c0 * H.lda, H.lda * 8, c1 * 8,
+                                          c1 - c0, cudaMemcpyHostToDevice, ss), "h2d A");
+                h2d += 8ull * c1 * (c1 - c0);
+                launch_pack_upper_col(da, (long long)m, Q.rcut, M, TSP, const_cast<double*>(Q.Apack), Q.anorm,
+                                      Q.aexp, k, ss);
+            }
+            if (t < N) {  // B tile column t (upper part) and C tile column t, from the left
+                const size_t c0 = PL.cc[t], c1 = PL.cc[t + 1];
+                ck(ctx, cudaMemcpy2DAsync(db + c0 * n, n * 8, H.b + c0 * H.ldb, H.ldb * 8, c1 * 8,
+                                          c1 - c0, cudaMemcpyHostToDevice, ss), "h2d B");
+                ck(ctx, cudaMemcpy2DAsync(dc + c0 * m, m * 8, H.c + c0 * H.ldc, H.ldc * 8, m * 8,
+                                          c1 - c0, cudaMemcpyHostToDevice, ss), "h2d C");
+                h2d += 8ull * c1 * (c1 - c0) + 8ull * m * (c1 - c0);
+                launch_pack_upper_col(db, (long long)n, Q.ccut, N, TSP, const_cast<double*>(Q.Bpack), Q.bnorm,
+                                      Q.bexp, t, ss);
+                launch_pack_full_col(dc, (long long)m, Q, Q.ynorm, t, ss);
+            }
+            launch_validate_col(Q, PL.d_reason, t < M ? M - 1 - t : -1, t < N ? t : -1,
+                                t < N ? t : -1, ss);
+            launch_set_ready(Q.in_ready, t < M ? t + 1 : -1, t < N ? t + 1 : -1,
+                             t < N ? t + 1 : -1, ss);
+        }
+        launch_persistent(Q, std::min(kPipeReserve, ctx->sms - 1), ss);
+        ck(ctx, cudaGetLastError(), "pipeline");
+        ck(ctx, cudaEventRecord(ctx->ev_side, ss), "event");
+    };
+    int emin = 0;
+    double numax = 0.0;
+    status = plan_run(ctx, H.res, &emin, &numax, &side);
+    H.res->h2d_bytes = h2d;
+    if (status != RSYLV_OK) return status;
+    const int ae = alpha_exponent(emin, numax, PL.omega);
+    status = plan_finish(ctx, ae, numax, emin, dy, m, H.res);
+    ck(ctx, cudaMemcpy2DAsync(H.y, H.ldy * 8, dy, m * 8, m * 8, n, cudaMemcpyDeviceToHost, st), "d2h Y");
+    ck(ctx, cudaStreamSynchronize(st), "sync");
+    H.res->d2h_bytes = 8ull * m * n;
+    return status;
+}
+
 static int solve_host_impl(rsylv_b200_ctx* ctx, const SolveArgs& H) {
     cudaStream_t st = H.st;
     const size_t m = H.m, n = H.n;
@@ -623,6 +751,14 @@ static int solve_host_impl(rsylv_b200_ctx* ctx, const SolveArgs& H) {
     double* db = buf<double>(ctx, "hB", n * n);
     double* dc = buf<double>(ctx, "hC", m * n);
     double* dy = buf<double>(ctx, "hY", m * n);
+    {   // host pipeline: on request, or automatically from 64 tiles up (single GPU, persistent)
+        const size_t ts = std::min<size_t>(std::max<size_t>(2, H.opt.tile_size), (size_t)kTileMax);
+        const size_t tiles = ((m + ts - 1) / ts) * ((n + ts - 1) / ts);
+        const bool pipe = H.opt.host_pipeline > 0 ||
+                          (H.opt.host_pipeline == 0 && tiles >= 64);
+        if (pipe && H.opt.scheduler == 0 && H.opt.virtual_ranks <= 1 && H.opt.tile_size >= 2)
+            return solve_host_pipelined(ctx, H, da, db, dc, dy);
+    }
     unsigned long long h2d = 8ull * m * n;
     // A and B are quasi-upper-triangular: only the upper tiles travel (tile column k needs rows
     // 0 .. end of tile k), halving their PCIe traffic; pack_upper never reads below them.
