@@ -156,7 +156,7 @@ int rsylv_b200_robust_update(rsylv_b200_ctx* ctx, size_t m, size_t k, size_t n, 
 
 /* Development counters: accumulated cycles per tile-task phase over all tasks since the last
  * reset (0 update GEMM, 1 solve setup, 2 sub-block solves, 3 in-tile updates, 4 finalize). */
-int rsylv_b200_debug_counters(unsigned long long* out16, int reset);
+int rsylv_b200_debug_counters(unsigned long long* out32, int reset);
 /* Development: average cycles of one warp-level 16x16 sub-block solve (mode bit 0: 2x2 blocks,
  * bit 1: force the exact solver); out256 (nullable) receives the solution, column-major. */
 int rsylv_b200_debug_subsolve(int reps, int mode, long long* cycles, double* out256);

@@ -12,10 +12,14 @@
 
 namespace rsb {
 
-constexpr int kSub = 16;         // sub-block edge inside a diagonal-tile solve (<= warp width)
+#ifndef RSYLV_KSUB
+#define RSYLV_KSUB 16
+#endif
+constexpr int kSub = RSYLV_KSUB; // sub-block edge inside a diagonal-tile solve (8 or 16)
 constexpr int kBM = 128;         // internal tile edge: one CTA task owns one <= 128 x 128 tile
 constexpr int kTileMax = kBM;    // largest internal tile edge
-constexpr int kSubMax = 9;       // max sub-blocks per tile edge (tile <= 128, sub-blocks >= 15)
+// max sub-blocks per tile edge (tile <= 128, sub-blocks >= kSub - 1)
+constexpr int kSubMax = (kBM + kSub - 2) / (kSub - 1);
 constexpr int kLDT = kBM + 1;    // shared-memory tile leading dim (odd: conflict-free columns)
 constexpr int kLDD = kSub + 1;   // staged diagonal sub-block leading dim
 constexpr int kMaxRanks = 8;     // GPUs (or virtual ranks) sharing one solve
@@ -23,6 +27,7 @@ constexpr int kKC = 32;          // K depth of one pipeline stage
 constexpr int kStages = 3;       // cp.async pipeline depth
 constexpr int kThreads = 512;    // 16 warps, for both task kinds
 constexpr int kWarps = kThreads / 32;
+constexpr int kSolvers = kSubMax < kWarps ? kSubMax : kWarps;  // warps solving sub-blocks at once
 constexpr int kLDA = kBM + 4;    // smem A stage: [kKC][kLDA] (rows contiguous), conflict-free
 constexpr int kLDB = kKC + 4;    // smem B stage: [kBM][kLDB] (k contiguous), conflict-free
 

@@ -1026,9 +1026,9 @@ int rsylv_b200_robust_update(rsylv_b200_ctx* ctx, size_t m, size_t k, size_t n, 
 }
 
 // development: per-phase cycle counters of the tile tasks (reset=1 clears them)
-int rsylv_b200_debug_counters(unsigned long long* out16, int reset) {
+int rsylv_b200_debug_counters(unsigned long long* out32, int reset) {
     if (reset) return reset_prof() == cudaSuccess ? RSYLV_OK : RSYLV_CUDA_ERROR;
-    return read_prof(out16) == cudaSuccess ? RSYLV_OK : RSYLV_CUDA_ERROR;
+    return read_prof(out32) == cudaSuccess ? RSYLV_OK : RSYLV_CUDA_ERROR;
 }
 
 // development: average cycles of one warp-level 16x16 sub-block solve (mixed: 2x2 blocks)

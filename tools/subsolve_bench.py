@@ -14,7 +14,7 @@ for mixed in (0, 1):
     for exact in (0, 1):
         cyc = C.c_longlong(0)
         out = np.zeros(256)
-        cnt = (C.c_uint64 * 16)()
+        cnt = (C.c_uint64 * 32)()
         L.rsylv_b200_debug_counters(cnt, 1)
         L.rsylv_b200_debug_subsolve(reps, mixed | (exact << 1), C.byref(cyc), out.ctypes.data_as(C.POINTER(C.c_double)))
         L.rsylv_b200_debug_counters(cnt, 0)

@@ -16,7 +16,7 @@ for rep in range(3):
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     flops = 0
     for b in range(sms):
-        i, j = b % 8, max(0, N - 2 - (b // 8) % 4)
+        i, j = (b % M, b % N) if os.environ.get("UB_DISTINCT") else (b % 8, max(0, N - 2 - (b // 8) % 4))
         nsrc = (M - 1 - i) + j
         flops += 2 * 128 * 128 * 128 * nsrc
     print(f"{name}: update-only {res.dag_ms:.2f} ms, {flops / res.dag_ms / 1e9:.2f} TFLOP/s "
