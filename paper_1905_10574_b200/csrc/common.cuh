@@ -27,6 +27,7 @@ constexpr int kKC = 32;          // K depth of one pipeline stage
 constexpr int kStages = 3;       // cp.async pipeline depth
 constexpr int kThreads = 512;    // 16 warps, for both task kinds
 constexpr int kWarps = kThreads / 32;
+constexpr int kYNormExp = 500;   // solved Y tiles are stored with norm in [2^499, 2^500)
 constexpr int kSolvers = kSubMax < kWarps ? kSubMax : kWarps;  // warps solving sub-blocks at once
 constexpr int kLDA = kBM + 4;    // smem A stage: [kKC][kLDA] (rows contiguous), conflict-free
 constexpr int kLDB = kKC + 4;    // smem B stage: [kBM][kLDB] (k contiguous), conflict-free
@@ -260,6 +261,8 @@ struct Problem {
     int* bexp;                  // N*N: the same for B
     double* ynorm;              // M*N current cached tile norm
     int* yexp;                  // M*N tile exponent (scale = 2^yexp, yexp <= 0)
+    int* yst;                   // M*N (= yexp + M*N): a solved tile is stored as Y_ij * 2^-yst,
+                                // normalized (norm in [2^(kYNormExp-1), 2^kYNormExp))
     int* uexp;                  // M*N exponent after the update phase
     double* ubnd;               // M*N update-phase growth bound (cached norm at rest)
     int* state;                 // M*N: 1 once solved (persistent scheduler flags)

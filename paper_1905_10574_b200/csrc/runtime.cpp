@@ -267,7 +267,7 @@ int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std:
         RankBufs& B = PL.rb[li];
         B.Yp = buf<double>(ctx, ("Ypack" + sfx).c_str(), ny * slot + slack);
         B.ynorm = buf<double>(ctx, ("ynorm" + sfx).c_str(), ny);
-        B.yexp = buf<int>(ctx, ("yexp" + sfx).c_str(), ny);
+        B.yexp = buf<int>(ctx, ("yexp" + sfx).c_str(), 2 * ny);  // yexp, then yst
         B.uexp = buf<int>(ctx, ("uexp" + sfx).c_str(), ny);
         B.ubnd = buf<double>(ctx, ("ubnd" + sfx).c_str(), ny);
         B.state = buf<int>(ctx, ("state" + sfx).c_str(), ny);
@@ -285,6 +285,7 @@ int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std:
         Q.Ypack = B.Yp;
         Q.ynorm = B.ynorm;
         Q.yexp = B.yexp;
+        Q.yst = B.yexp + ny;
         Q.uexp = B.uexp;
         Q.state = B.state;
         Q.udone = B.udone;
@@ -344,6 +345,7 @@ Problem rank_problem(rsylv_b200_ctx* ctx, size_t li) {
     Q.Ypack = B.Yp;
     Q.ynorm = B.ynorm;
     Q.yexp = B.yexp;
+    Q.yst = B.yexp + (size_t)Q.M * Q.N;
     Q.uexp = B.uexp;
     Q.ubnd = B.ubnd;
     Q.state = B.state;
@@ -945,7 +947,7 @@ int rsylv_b200_robust_update(rsylv_b200_ctx* ctx, size_t m, size_t k, size_t n, 
         int* ax = buf<int>(ctx, "ruax", 4);
         int* bx = buf<int>(ctx, "rubx", 1);
         double* yn = buf<double>(ctx, "ruyn", 2);
-        int* ye = buf<int>(ctx, "ruye", 2);
+        int* ye = buf<int>(ctx, "ruye", 4);  // yexp, then yst
         int* ue = buf<int>(ctx, "ruue", 2);
         double* ub = buf<double>(ctx, "ruub", 2);
         int* sta = buf<int>(ctx, "rust", 2);
@@ -981,6 +983,7 @@ int rsylv_b200_robust_update(rsylv_b200_ctx* ctx, size_t m, size_t k, size_t n, 
         P.bexp = bx;
         P.ynorm = yn;
         P.yexp = ye;
+        P.yst = ye + 2;
         P.uexp = ue;
         P.ubnd = ub;
         P.state = sta;
