@@ -23,7 +23,6 @@ for name in sys.argv[1:] or ["c1"]:
     print("   column-path fallbacks to the exact sub-block solver: %d" % out[12])
     print("   flag-wait=%.1f us/tile, metadata-arrival=%.1f us/tile, header=%.1f us/tile, chunks=%d prescaled=%d (%.1f%%)" % (out[9] / ntiles / 1965, out[14] / ntiles / 1965, out[13] / ntiles / 1965, out[10], out[11], 100.0 * out[11] / max(1, out[10])))
     nw = ntiles * 16 * 1965
-    print("   fresh sources %d, lookahead hits %d (%.1f%%); prescaled down %d / up %d" % (out[16], out[17], 100.0 * out[17] / max(1, out[16]), out[21], out[22]))
-    print("   per warp per tile: cp.async wait %.1f us, pre-scale %.1f us, barrier %.1f us, issue %.1f us, mma %.1f us" % tuple(out[k] / nw for k in (18, 19, 20, 23, 24)))
+    print("   chunks with an accumulator shift %d (%.1f%%), skipped (not live) %d" % (out[18], 100.0 * out[18] / max(1, out[10]), out[19]))
     print(name, "dag_ms", round(res.dag_ms, 2), "tiles", ntiles, " ".join(
         f"{names[i]}={out[i] / ntiles / 1965:.1f}us({100 * out[i] / tot:.0f}%)" for i in range(5)))
