@@ -175,6 +175,23 @@ def test_baseline_twins_vs_live_reference(name, m, n, t):
     assert res <= 16 * m * n * np.finfo(float).eps
 
 
+@pytest.mark.parametrize("t", [256, 512])
+def test_c5_twin_with_scaling_vs_live_reference(t):
+    """BASELINE config-5 distributions (50 % 2x2 blocks, one C tile x 1e250) at 1280^2: the
+    reference solves it WITH robust scaling (alpha = 7.9e-6 at tile 256, 3.3e-20 at tile 512,
+    probed with configs.host_system), so Y/alpha of the scaling path is compared directly."""
+    from paper_1905_10574_b200.configs import CONFIGS, host_system
+    cfg = CONFIGS["c5"].scaled(1280, 1280, t)
+    a, ac, b, bc, c = host_system(cfg)
+    ref = po.solve_tiled(a, ac, b, bc, c, t, impl="ref", workers=os.cpu_count() or 1)
+    assert ref.status == 0 and 0.0 < ref.alpha < 1e-5
+    st, r = gpu_solve(dict(a=a, ab=ac, b=b, bb=bc, c=c, tile=t, omega=0.0))
+    assert STATUS[st] == STATUS[ref.status]
+    assert np.isfinite(r.y).all() and r.alpha_exp < 0
+    assert unscaled_ratio_err(r.y, r.alpha_exp, ref.y, ref.alpha) <= 1e-10
+    assert po.relative_residual_safe(a, b, c, r.y, 1.0, r.alpha_exp) <= 16 * 1280 * 1280 * np.finfo(float).eps
+
+
 @pytest.mark.parametrize("m,n,t", [(0, 5, 4), (5, 0, 4), (1, 1, 2), (2, 2, 2), (3, 2, 1000),
                                     (37, 41, 1100), (130, 3, 128)])
 def test_edge_shapes(m, n, t):
