@@ -13,15 +13,18 @@ cudaError_t read_prof(unsigned long long* out);
 cudaError_t reset_prof();
 cudaError_t configure_kernels();
 
+// normalize = false (the non-robust solve, omega = +inf): off-diagonal tiles stored unscaled
 void launch_pack_upper(const double* src, long long ld, const int* cut, int T, int TSP,
-                       double* dst, double* norms, int* sexp, cudaStream_t st);
+                       double* dst, double* norms, int* sexp, cudaStream_t st,
+                       bool normalize = true);
 void launch_pack_full(const double* src, long long ld, const Problem& P, double* norms,
                       cudaStream_t st);
 void launch_tile_diag(const Problem& P, int d, int ntiles, cudaStream_t st);
 void launch_update_only(const Problem& P, int i, int j, cudaStream_t st);
 void launch_update_bench(const Problem& P, int ctas, cudaStream_t st);
 void launch_pack_upper_col(const double* src, long long ld, const int* cut, int T, int TSP,
-                           double* dst, double* norms, int* sexp, int k, cudaStream_t st);
+                           double* dst, double* norms, int* sexp, int k, cudaStream_t st,
+                           bool normalize = true);
 void launch_pack_full_col(const double* src, long long ld, const Problem& P, double* norms,
                           int j, cudaStream_t st);
 void launch_set_ready(int* ready, int a, int b, int c, cudaStream_t st);

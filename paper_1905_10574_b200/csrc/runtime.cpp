@@ -255,8 +255,10 @@ int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std:
         ck(ctx, cudaMemcpyAsync(PL.d_reason, &four, sizeof(int), cudaMemcpyHostToDevice, st), "h2d");
         P.in_ready = rdy;
     } else {
-        launch_pack_upper(A.a, (long long)A.lda, d_rc, M, TSP, Ap, anorm, aexp, st);
-        launch_pack_upper(A.b, (long long)A.ldb, d_cc, N, TSP, Bp, bnorm, bexp, st);
+        launch_pack_upper(A.a, (long long)A.lda, d_rc, M, TSP, Ap, anorm, aexp, st,
+                          !std::isinf(PL.omega));
+        launch_pack_upper(A.b, (long long)A.ldb, d_cc, N, TSP, Bp, bnorm, bexp, st,
+                          !std::isinf(PL.omega));
     }
 
     PL.rb.assign(local.size(), RankBufs{});
@@ -711,7 +713,7 @@ static int solve_host_pipelined(rsylv_b200_ctx* ctx, const SolveArgs& H, double*
                                           c1 - c0, cudaMemcpyHostToDevice, ss), "h2d A");
                 h2d += 8ull * c1 * (c1 - c0);
                 launch_pack_upper_col(da, (long long)m, Q.rcut, M, TSP, const_cast<double*>(Q.Apack), Q.anorm,
-                                      Q.aexp, k, ss);
+                                      Q.aexp, k, ss, !std::isinf(PL.omega));
             }
             if (t < N) {  // B tile column t (upper part) and C tile column t, from the left
                 const size_t c0 = PL.cc[t], c1 = PL.cc[t + 1];
@@ -721,7 +723,7 @@ static int solve_host_pipelined(rsylv_b200_ctx* ctx, const SolveArgs& H, double*
                                           c1 - c0, cudaMemcpyHostToDevice, ss), "h2d C");
                 h2d += 8ull * c1 * (c1 - c0) + 8ull * m * (c1 - c0);
                 launch_pack_upper_col(db, (long long)n, Q.ccut, N, TSP, const_cast<double*>(Q.Bpack), Q.bnorm,
-                                      Q.bexp, t, ss);
+                                      Q.bexp, t, ss, !std::isinf(PL.omega));
                 launch_pack_full_col(dc, (long long)m, Q, Q.ynorm, t, ss);
             }
             launch_validate_col(Q, PL.d_reason, t < M ? M - 1 - t : -1, t < N ? t : -1,
@@ -996,7 +998,7 @@ int rsylv_b200_robust_update(rsylv_b200_ctx* ctx, size_t m, size_t k, size_t n, 
         P.small_num = DBL_MIN / DBL_EPSILON;
         P.x_omega = host_xf(P.omega);
         P.x_target = host_xf(P.omega * (1.0 - 0x1p-30));
-        launch_pack_upper(dA, (long long)mk, d_rc, M, TSP, Ap, an, ax, st);
+        launch_pack_upper(dA, (long long)mk, d_rc, M, TSP, Ap, an, ax, st, !std::isinf(P.omega));
         ck(ctx, cudaMemsetAsync(bx, 0, sizeof(int), st), "memset");
         launch_pack_full(dY, (long long)mk, P, yn, st);
         const int exps[2] = {c_exp ? *c_exp : 0, ab_exp};

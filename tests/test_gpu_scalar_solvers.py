@@ -36,6 +36,27 @@ def test_nonrobust_overflows_like_the_reference():
     assert np.isfinite(y).sum() == np.isfinite(ref.y).sum() or not np.isfinite(y).all()
 
 
+@pytest.mark.parametrize("n", [128, 200, 300])
+def test_nonrobust_inf_propagates_through_tiles(n):
+    """Non-robust (omega = +inf) on a growth system that overflows, over several 128-tiles: no
+    guard may fire and nothing may be rescaled, so the entries the reference's plain substitution
+    keeps finite come out equal (the engine's exponent-form accumulation avoids some of the
+    reference's intermediate overflows, so it may keep MORE entries finite, never markedly fewer).
+    """
+    import paper_1905_10574_b200 as rs
+    a, ac = po.ref_generate_quasi_triangular(n, 1e-3)
+    b, bc = po.ref_generate_quasi_triangular(n, 1e-2)
+    c = np.ones((n, n))
+    y = rs.solve_nonrobust(qt(a, ac), qt(b, bc), c)
+    ref = po.solve_nonrobust(a, ac, b, bc, c, impl="ref")
+    fg, fr = np.isfinite(y), np.isfinite(ref.y)
+    assert not fr.all() and not fg.all()
+    assert (fr & ~fg).sum() <= 0.01 * fr.sum()
+    both = fg & fr & (np.abs(ref.y) > 0)
+    rel = np.abs(y[both] - ref.y[both]) / np.abs(ref.y[both])
+    assert np.median(rel) <= 1e-10 and np.quantile(rel, 0.9) <= 1e-8
+
+
 def test_nonrobust_singular():
     import paper_1905_10574_b200 as rs
     d = CASES["singular_n8"]
