@@ -67,3 +67,22 @@ def test_host_pipeline_bitwise_deterministic():
     e0, y0 = outs[0]
     for e, y in outs[1:]:
         assert e == e0 and np.array_equal(y, y0)
+
+
+def test_c5_full_size_bitwise_deterministic():
+    """The benchmark workload itself (config 5, 40000^2, 6241 nominal tiles, 98596 tile tasks on
+    148 SMs): three solves, compared on the device (Y is 12.8 GB)."""
+    import torch
+    from paper_1905_10574_b200 import api
+    from paper_1905_10574_b200.configs import CONFIGS, device_system
+    cfg = CONFIGS["c5"]
+    A, ac, B, bc, C = device_system(cfg, torch)
+    Y0 = torch.empty((cfg.n, cfg.m), dtype=torch.float64, device="cuda").T
+    st0, r0 = api.solve_tiled_robust_device(A, ac, B, bc, C, Y0, cfg.tile, raise_underflow=False)
+    Y1 = torch.empty_like(Y0)
+    for _ in range(2):
+        Y1.fill_(float("nan"))
+        st, r = api.solve_tiled_robust_device(A, ac, B, bc, C, Y1, cfg.tile, raise_underflow=False)
+        assert st == st0 and r.alpha_exp == r0.alpha_exp
+        # bitwise (int64 views: NaN-safe, -0.0 distinct)
+        assert torch.equal(Y1.view(torch.int64), Y0.view(torch.int64))
