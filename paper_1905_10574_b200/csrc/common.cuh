@@ -21,7 +21,8 @@ constexpr int kTileMax = kBM;    // largest internal tile edge
 // max sub-blocks per tile edge (tile <= 128, sub-blocks >= kSub - 1)
 constexpr int kSubMax = (kBM + kSub - 2) / (kSub - 1);
 constexpr int kLDT = kBM + 1;    // shared-memory tile leading dim (odd: conflict-free columns)
-constexpr int kLDD = kSub + 1;   // staged diagonal sub-block leading dim
+constexpr int kLDD = kSub + 1;   // staged diagonal sub-block of B leading dim (column reads across lanes)
+constexpr int kLDDA = kSub;      // staged diagonal sub-block of A: row reads across lanes (r0 + 16 c: distinct banks)
 constexpr int kMaxRanks = 8;     // GPUs (or virtual ranks) sharing one solve
 constexpr int kKC = 32;          // K depth of one pipeline stage
 constexpr int kStages = 3;       // cp.async pipeline depth
