@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--force-dist", action="store_true",
+                   help="run the multi-GPU path (dist.py, NCCL) even at N=1 (testing)")
     return p.parse_args()
 
 
@@ -168,8 +170,15 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    use_dist = world > 1 or args.force_dist  # --force-dist: the multi-GPU path at any N
     torch.cuda.set_device(local)
-    if world > 1:
+    json_out = sys.stdout
+    if use_dist:
+        # NCCL writes its banner ("NCCL version ...") to fd 1 when NCCL_DEBUG asks for it; keep
+        # stdout for the one JSON line and send everything else to stderr
+        sys.stdout.flush()
+        json_out = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1905_10574_b200 import api, _native as nat
     from paper_1905_10574_b200.configs import CONFIGS, device_system
@@ -180,7 +189,7 @@ def main():
     ocfg = api.OverflowConfig()
 
     def step():
-        if world > 1:
+        if use_dist:
             from paper_1905_10574_b200.dist import solve_dist
             st, _, res = solve_dist(A, ac, B, bc, Cm, Y, cfg.tile, ocfg, stream=stream.cuda_stream,
                                     device=local)
@@ -194,7 +203,7 @@ def main():
     for _ in range(args.warmup):
         st, res = step()
     torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -208,7 +217,7 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    if world > 1:
+    if use_dist:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -216,7 +225,7 @@ def main():
     torch.cuda.synchronize()
     ms_step = ms / args.steps
     value = cfg.flops() / (ms_step / 1e3) / 1e9  # one solve per step, split over the ranks
-    if world > 1:
+    if use_dist:
         own = [j for j in range(0, (cfg.n + 127) // 128) if j % world == rank]
         finite = all(bool(torch.isfinite(Y[:, j * 128:(j + 1) * 128]).all().item()) for j in own[:4])
     else:
@@ -225,7 +234,7 @@ def main():
 
     # e2e through the host API with pinned buffers
     e2e = None
-    if not args.no_e2e and args.e2e_steps > 0 and world == 1:
+    if not args.no_e2e and args.e2e_steps > 0 and not use_dist:
         # pinned host copies holding the column-major matrices (the storage of the .T views)
         hA = torch.empty((cfg.m, cfg.m), dtype=torch.float64, pin_memory=True)
         hB = torch.empty((cfg.n, cfg.n), dtype=torch.float64, pin_memory=True)
@@ -251,7 +260,7 @@ def main():
             dt = time.perf_counter() - t0
             if it > 0:  # first call warms the host-path staging buffers
                 times.append(dt)
-        if world > 1:
+        if use_dist:
             t = torch.tensor([max(times)], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             tmax = float(t.item())
@@ -298,7 +307,7 @@ def main():
                        "tile": cfg.tile, "scheduler": "persistent" if args.scheduler == 0
                        else "wavefront", "l2": "inputs 12.8 GB/matrix >> 126 MB L2, no flush",
                        "parallelism": (f"tile columns block-cyclic over {world} GPUs, NVLink "
-                                       "tile push + NCCL alpha all-reduce") if world > 1 else "1 GPU",
+                                       "tile push + NCCL alpha all-reduce") if use_dist else "1 GPU",
                        "alpha_exp": alpha_exp, "status": nat.lib().rsylv_b200_status_string(
                            statuses[-1]).decode(), "y_finite": finite,
                        "scaling_events": int(res.scaling_events)},
@@ -314,13 +323,13 @@ def main():
             "e2e": e2e,
             "e2e_note": None if e2e else ("not measured at N > 1: every rank would need pinned host "
                                           "copies of A, B and C (3 x 12.8 GB per rank at c5)"
-                                          if world > 1 else "disabled (--no-e2e)"),
+                                          if use_dist else "disabled (--no-e2e)"),
             "cpu_baseline": cpu,
             "gpu_launches": args.steps * (4 + int(res.dag_launches)),
             "breakdown_ms": {"pack": res.pack_ms, "dag": dag, "unpack": res.unpack_ms},
         }
-        print(json.dumps(line), flush=True)
-    if world > 1:
+        print(json.dumps(line), file=json_out, flush=True)
+    if use_dist:
         dist.destroy_process_group()
 
 
