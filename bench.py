@@ -160,14 +160,68 @@ def reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def maybe_relaunch(args) -> None:
+    """`python bench.py --gpus N` with N > 1 outside torchrun: re-exec this script under
+    torch.distributed.run with N processes (one per GPU), so that the number of GPUs measured is
+    the number asked for. Fails loudly when fewer than N devices are visible (never silently
+    measures fewer). RSYLV_BENCH_DRYRUN=1 runs the same launch on CPU with gloo ranks that only
+    report the world size (tests/test_bench_launch.py)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    dry = os.environ.get("RSYLV_BENCH_DRYRUN") == "1"
+    if not dry:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) "
+                             "are visible\n")
+            sys.exit(2)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def dry_run(args) -> None:
+    """RSYLV_BENCH_DRYRUN=1 under torchrun: a gloo all-reduce over the ranks the launcher
+    started; rank 0 prints {"dry_run": true, "n_gpus": world, "ranks": sum of ranks}."""
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo")
+    world, rank = dist.get_world_size(), dist.get_rank()
+    t = torch.tensor([rank], dtype=torch.int64)
+    dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "gpus_arg": args.gpus,
+                          "ranks": int(t.item())}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
+    maybe_relaunch(args)
+    if os.environ.get("RSYLV_BENCH_DRYRUN") == "1":
+        dry_run(args)
+        return
     if args.impl == "reference":
         reference_arm(args)
         return
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != max(1, args.gpus):
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        sys.exit(2)
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     use_dist = world > 1 or args.force_dist  # --force-dist: the multi-GPU path at any N
@@ -225,9 +279,10 @@ def main():
     torch.cuda.synchronize()
     ms_step = ms / args.steps
     value = cfg.flops() / (ms_step / 1e3) / 1e9  # one solve per step, split over the ranks
-    if use_dist:
-        own = [j for j in range(0, (cfg.n + 127) // 128) if j % world == rank]
-        finite = all(bool(torch.isfinite(Y[:, j * 128:(j + 1) * 128]).all().item()) for j in own[:4])
+    if use_dist:  # every owned tile column (the solver's own partition)
+        cuts = api.tile_cuts(bc, cfg.n, cfg.tile)
+        finite = all(bool(torch.isfinite(Y[:, cuts[j]:cuts[j + 1]]).all().item())
+                     for j in range(len(cuts) - 1) if j % world == rank)
     else:
         finite = bool(torch.isfinite(Y).all().item())
     alpha_exp = int(res.alpha_exp)
@@ -304,7 +359,8 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": f"{cfg.name}: {cfg.note}", "m": cfg.m, "n": cfg.n,
-                       "tile": cfg.tile, "scheduler": "persistent" if args.scheduler == 0
+                       "tile": cfg.tile, "internal_tile": min(cfg.tile, api.INTERNAL_TILE),
+                       "scheduler": "persistent" if args.scheduler == 0
                        else "wavefront", "l2": "inputs 12.8 GB/matrix >> 126 MB L2, no flush",
                        "parallelism": (f"tile columns block-cyclic over {world} GPUs, NVLink "
                                        "tile push + NCCL alpha all-reduce") if use_dist else "1 GPU",

@@ -56,7 +56,11 @@ enum {
 typedef struct {
     double omega;      /* OverflowConfig::omega (overflow.hpp:15); 0 -> DBL_MAX/2           */
     double small_num;  /* OverflowConfig::small_num (overflow.hpp:18); 0 -> DBL_MIN/eps      */
-    size_t tile_size;  /* requested tile size (>= 2); tiles above 1024 are split internally */
+    size_t tile_size;  /* requested tile size (>= 2). The device works on tiles of at most
+                          128 (one CTA per tile): a larger request is served by 128-tiles.
+                          alpha, scaling_events and the probe's (k, l) indices follow that
+                          internal partition (cut moved one index earlier around a 2x2 block);
+                          Y/alpha does not depend on it                                     */
     int scheduler;     /* 0: persistent dataflow kernel (default), 1: host-driven wavefront */
     int virtual_ranks; /* >1: emulate that many GPUs on this device (tile columns block-cyclic,
                           solved tiles pushed between per-rank workspaces) -- validates the

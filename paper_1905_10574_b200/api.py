@@ -157,6 +157,27 @@ class QuasiTriangular:
         return list(self._blocks)
 
 
+INTERNAL_TILE = 128  # largest internal tile edge (kTileMax in csrc/common.cuh)
+
+
+def tile_cuts(codes, n: int, tile_size: int) -> list:
+    """The B200 partition of an index range (mirror of partition() in csrc/runtime.cpp): cut at
+    running multiples of min(tile_size, 128); a cut that would split a 2x2 block moves one index
+    EARLIER (the reference moves it later, partition.cpp:74-91). alpha and the TileProbe
+    indices refer to these tiles."""
+    ts = min(max(2, int(tile_size)), INTERNAL_TILE)
+    cuts, pos = [0], 0
+    while pos < n:
+        nx = pos + ts
+        if nx >= n:
+            nx = n
+        elif codes is not None and codes[nx - 1] == 2:
+            nx -= 1
+        cuts.append(nx)
+        pos = nx
+    return cuts
+
+
 def _status_to_exc(st: int, res: nat.Result, partial: "SolveResult | None" = None):
     if st == nat.RSYLV_INVALID_ARGUMENT:
         return ValueError("solve_tiled_robust: " + nat.REASONS.get(res.invalid_reason, "invalid"))

@@ -135,6 +135,7 @@ struct Plan {
     cudaStream_t st = nullptr;
     int scheduler = 0;
     rsylv_b200_probe_event* d_probe = nullptr;
+    unsigned long long probe_cap = 0;
     int* d_reason = nullptr;  // host pipeline: first failing argument check (device)
 };
 
@@ -308,8 +309,11 @@ int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std:
             ck(ctx, cudaMemcpyAsync(B.tasks, T.data(), sizeof(int) * T.size(), cudaMemcpyHostToDevice, st), "h2d");
         ck(ctx, cudaStreamSynchronize(st), "sync");  // T goes out of scope
     }
-    if (res->probe_log && res->probe_cap && nranks == 1)
+    PL.probe_cap = 0;
+    if (res->probe_log && res->probe_cap && nranks == 1) {
         PL.d_probe = buf<rsylv_b200_probe_event>(ctx, "probe", res->probe_cap);
+        PL.probe_cap = res->probe_cap;
+    }
     ck(ctx, cudaGetLastError(), "pack");
 
     if (deferred) return RSYLV_OK;  // validated on the device after the last pack
@@ -365,7 +369,7 @@ Problem rank_problem(rsylv_b200_ctx* ctx, size_t li) {
     if (PL.d_probe) {
         Q.probe = reinterpret_cast<ProbeEv*>(PL.d_probe);
         Q.probe_count = B.ev + 1;
-        Q.probe_cap = 0;
+        Q.probe_cap = PL.probe_cap;  // every launch of the solve (main and side streams) logs
     }
     if (PL.nranks > 1) {
         if (PL.local.size() > 1) {  // virtual ranks on this device
@@ -409,7 +413,6 @@ int plan_run(rsylv_b200_ctx* ctx, rsylv_b200_result* res, int* emin_out, double*
     ck(ctx, cudaEventRecord(ctx->evp, st), "event");
     if (PL.nranks == 1) {
         Problem P = rank_problem(ctx, 0);
-        if (PL.d_probe) P.probe_cap = res->probe_cap;
         if (PL.scheduler == 2) {  // development: update-phase throughput (garbage results)
             launch_update_bench(P, ctx->sms, st);
             res->dag_launches = 1;
@@ -421,10 +424,14 @@ int plan_run(rsylv_b200_ctx* ctx, rsylv_b200_result* res, int* emin_out, double*
                 res->dag_launches += 1;
             }
         } else if (side) {
-            // the side stream starts after the setup on st, NOT after the DAG launched below
+            // the side stream starts after the setup on st, NOT after the DAG launched below.
+            // Every producer (H2D, pack, validation, ready counters) is enqueued BEFORE the
+            // spinning DAG kernel: its progress then never depends on the two streams running
+            // concurrently (CUDA_LAUNCH_BLOCKING=1, compute-sanitizer or an MPS SM cap serialize
+            // them; the side stream's own DAG CTAs then solve everything)
             ck(ctx, cudaEventRecord(ctx->ev_side0, st), "event");
-            launch_persistent(P, std::max(1, ctx->sms - kPipeReserve), st);
             (*side)();
+            launch_persistent(P, std::max(1, ctx->sms - kPipeReserve), st);
             ck(ctx, cudaStreamWaitEvent(st, ctx->ev_side, 0), "join");
             res->dag_launches = 2;
         } else {
@@ -655,6 +662,13 @@ void rsylv_b200_destroy(rsylv_b200_ctx* ctx) {
     delete ctx;
 }
 
+// The stream argument of the device-resident entry points: NULL is the legacy default stream
+// (include/rsylv_b200.h), so the solve is ordered after the caller's work on it (torch's
+// default stream handle is 0).
+static cudaStream_t as_stream(void* stream) {
+    return stream ? (cudaStream_t)stream : cudaStreamLegacy;
+}
+
 static void init_result(rsylv_b200_result* r) {
     rsylv_b200_probe_event* log = r->probe_log;
     size_t cap = r->probe_cap;
@@ -671,8 +685,7 @@ int rsylv_b200_solve_device(rsylv_b200_ctx* ctx, size_t m, size_t n, const doubl
     if (!ctx || !opt || !res) return RSYLV_INVALID_ARGUMENT;
     init_result(res);
     if (cudaSetDevice(ctx->device) != cudaSuccess) return RSYLV_CUDA_ERROR;
-    SolveArgs A{m, n, a, b, c, lda, ldb, ldc, ablk, bblk, y, ldy, *opt,
-                stream ? (cudaStream_t)stream : ctx->own_stream, res};
+    SolveArgs A{m, n, a, b, c, lda, ldb, ldc, ablk, bblk, y, ldy, *opt, as_stream(stream), res};
     return guarded_call(ctx, solve_device_impl, A);
 }
 
@@ -835,8 +848,8 @@ int rsylv_b200_dist_prepare(rsylv_b200_ctx* ctx, int nranks, int rank, size_t m,
     if (m == 0 || n == 0) return RSYLV_INVALID_ARGUMENT;
     if (cudaSetDevice(ctx->device) != cudaSuccess) return RSYLV_CUDA_ERROR;
     try {
-        SolveArgs A{m, n, a, b, c, lda, ldb, ldc, ablk, bblk, nullptr, 0, *opt,
-                    stream ? (cudaStream_t)stream : ctx->own_stream, res};
+        SolveArgs A{m, n, a, b, c, lda, ldb, ldc, ablk, bblk, nullptr, 0, *opt, as_stream(stream),
+                    res};
         A.opt.scheduler = 0;
         const int st = plan_prepare(ctx, A, nranks, std::vector<int>{rank});
         if (st != RSYLV_OK) return st;
@@ -860,7 +873,7 @@ int rsylv_b200_dist_run(rsylv_b200_ctx* ctx, const void* all_handles, void* stre
     if (cudaSetDevice(ctx->device) != cudaSuccess) return RSYLV_CUDA_ERROR;
     try {
         Plan& PL = ctx_plan(ctx);
-        if (stream) PL.st = (cudaStream_t)stream;
+        PL.st = as_stream(stream);
         rsylv_b200_plan_holder& H = ctx_holder(ctx);
         const unsigned char* in = static_cast<const unsigned char*>(all_handles);
         const int R = PL.nranks, me = PL.local[0];
@@ -902,7 +915,7 @@ int rsylv_b200_dist_finish(rsylv_b200_ctx* ctx, int alpha_exp, double* y, size_t
     if (cudaSetDevice(ctx->device) != cudaSuccess) return RSYLV_CUDA_ERROR;
     try {
         Plan& PL = ctx_plan(ctx);
-        if (stream) PL.st = (cudaStream_t)stream;
+        PL.st = as_stream(stream);
         // res->alpha_exp / max_tile_norm on entry: the global emin and numax (relative to emin)
         const int emin = res->alpha_exp;
         const double numax = res->max_tile_norm;

@@ -5,7 +5,7 @@ to_csv_row, parse_csv_row, write_csv, read_csv) and src/matrix_io.cpp:10-67 (for
 parse_double, write_matrix / read_matrix and the *_file variants). Numbers are written as the
 SHORTEST round-trip decimal exactly like std::to_chars (fixed or scientific, whichever is
 shorter, fixed on a tie), so a CSV written here is byte-identical to the reference's for equal
-values and a reparse reproduces every value bitwise (tests/test_records.py pins the format
+values and a reparse reproduces every value bitwise (tests/test_cli_host.py pins the format
 against the reference's own format_double).
 """
 from __future__ import annotations

@@ -82,3 +82,53 @@ def test_pipeline_reuse_after_failure():
         api.solve_tiled_robust(qt(a, ac), qt(b, bc), bad, 64, host_pipeline=1)
     r0, r1 = _both(a, ac, b, bc, c, 64)
     assert np.array_equal(r0.y, r1.y)
+
+
+@pytest.mark.parametrize("hp", [1, -1])
+def test_probe_log_complete_with_pipeline(hp):
+    """Every tile at rest is reported exactly once by the TileProbe (tiled_solve.hpp:24-27),
+    also by the DAG CTAs the host pipeline launches on its side stream (>= 64 tiles)."""
+    cfg = CONFIGS["c5"].scaled(1100, 1030, 128)
+    a, ac, b, bc, c = host_system(cfg)
+    ev = []
+    r = api.solve_tiled_robust(qt(a, ac), qt(b, bc), c, 128, host_pipeline=hp,
+                               probe=lambda k, l, s, nr: ev.append((k, l, s, nr)))
+    rc, cc = api.tile_cuts(ac, cfg.m, 128), api.tile_cuts(bc, cfg.n, 128)
+    M, N = len(rc) - 1, len(cc) - 1
+    assert M * N >= 64
+    keys = sorted((k, l) for k, l, _, _ in ev)
+    assert keys == sorted((k, l) for k in range(M) for l in range(N)), "missing/duplicate tiles"
+    assert all(0.0 <= nr <= api.default_omega() and 0.0 <= s <= 1.0 for _, _, s, nr in ev)
+
+
+def test_pipeline_survives_serialized_launches():
+    """CUDA_LAUNCH_BLOCKING=1 serializes the streams: the host pipeline enqueues every producer
+    before the spinning DAG kernel, so the solve still completes (no watchdog) and is bitwise
+    the concurrent result."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_1905_10574_b200 import api
+from paper_1905_10574_b200.configs import CONFIGS, host_system
+cfg = CONFIGS["c5"].scaled(1100, 1030, 128)
+a, ac, b, bc, c = host_system(cfg)
+r = api.solve_tiled_robust(api.QuasiTriangular.from_codes(a, ac), api.QuasiTriangular.from_codes(b, bc), c, 128, host_pipeline=1)
+np.save(sys.argv[2], r.y)
+print(r.alpha_exp)
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = os.path.join(root, "gpurun_out", "serialized_y.npy")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    env = dict(os.environ, CUDA_LAUNCH_BLOCKING="1")
+    p = subprocess.run([sys.executable, "-c", code, root, out], env=env, capture_output=True,
+                       text=True, timeout=300)
+    assert p.returncode == 0, p.stderr[-3000:]
+    cfg = CONFIGS["c5"].scaled(1100, 1030, 128)
+    a, ac, b, bc, c = host_system(cfg)
+    r = api.solve_tiled_robust(qt(a, ac), qt(b, bc), c, 128, host_pipeline=1)
+    assert int(p.stdout.split()[-1]) == r.alpha_exp
+    assert np.array_equal(np.load(out), r.y)
+    os.remove(out)
