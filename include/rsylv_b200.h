@@ -68,6 +68,10 @@ typedef struct {
     int host_pipeline; /* rsylv_b200_solve only: stream the inputs in (H2D + pack per tile
                           column) while the solve runs. 0: automatic (from 64 tiles),
                           1: always, -1: never (copy everything first)                     */
+    int fast_diag;     /* diagonal-tile solves: 0 (default) = the exact exponent-form sub-block
+                          path; 1 = a plain-FP64 attempt on the power-of-two normalized tile
+                          first (tiles of 1x1 blocks), the exact path only when a pivot /
+                          range check fails (Y/alpha agree to rounding either way)          */
 } rsylv_b200_options;
 
 /* One TileProbe event (tiled_solve.hpp:24-27): tile (k, l) came to rest with local scale

@@ -23,7 +23,8 @@ REASONS = {0: "", 1: "C does not conform with A and B", 2: "tile size must be >=
 
 class Options(C.Structure):
     _fields_ = [("omega", C.c_double), ("small_num", C.c_double), ("tile_size", C.c_size_t),
-                ("scheduler", C.c_int), ("virtual_ranks", C.c_int), ("host_pipeline", C.c_int)]
+                ("scheduler", C.c_int), ("virtual_ranks", C.c_int), ("host_pipeline", C.c_int),
+                ("fast_diag", C.c_int)]
 
 
 class ProbeEvent(C.Structure):

@@ -205,7 +205,7 @@ def solve_tiled_robust(a: QuasiTriangular, b: QuasiTriangular, c, tile_size: int
                        probe: Optional[Callable[[int, int, float, float], None]] = None,
                        scheduler: int = 0, device: int = 0,
                        probe_capacity: int = 1 << 20, virtual_ranks: int = 1,
-                       host_pipeline: int = 0) -> SolveResult:
+                       host_pipeline: int = 0, fast_diag: bool = False) -> SolveResult:
     """Solves A*Y + Y*B = alpha*C with every tile of Y bounded by cfg.omega (tiled_solve.hpp:29-40).
 
     HOST arrays in, HOST array out (the reference calling convention). ``mode.workers`` is the
@@ -220,7 +220,7 @@ def solve_tiled_robust(a: QuasiTriangular, b: QuasiTriangular, c, tile_size: int
     cf = np.asfortranarray(c)
     y = np.zeros((m, n), order="F")
     opt = nat.Options(cfg.omega, cfg.small_num, int(tile_size), scheduler, int(virtual_ranks),
-                      int(host_pipeline))
+                      int(host_pipeline), int(bool(fast_diag)))
     res = nat.Result()
     pbuf = None
     if probe is not None:
@@ -244,7 +244,7 @@ def solve_tiled_robust(a: QuasiTriangular, b: QuasiTriangular, c, tile_size: int
 def solve_tiled_robust_device(a_dev, a_codes, b_dev, b_codes, c_dev, y_dev, tile_size: int,
                               cfg: Optional[OverflowConfig] = None, stream=None,
                               scheduler: int = 0, device: int = 0, raise_underflow=True,
-                              virtual_ranks: int = 1):
+                              virtual_ranks: int = 1, fast_diag: bool = False):
     """Device-resident variant: torch CUDA tensors (column-major, i.e. ``t.T.contiguous().T``
     or any tensor whose stride(0) == 1). Returns (status, nat.Result)."""
     cfg = cfg or OverflowConfig()
@@ -252,7 +252,8 @@ def solve_tiled_robust_device(a_dev, a_codes, b_dev, b_codes, c_dev, y_dev, tile
     for t in (a_dev, b_dev, c_dev, y_dev):
         if t.stride(0) != 1:
             raise ValueError("device arrays must be column-major (stride(0) == 1)")
-    opt = nat.Options(cfg.omega, cfg.small_num, int(tile_size), scheduler, int(virtual_ranks))
+    opt = nat.Options(cfg.omega, cfg.small_num, int(tile_size), scheduler, int(virtual_ranks), 0,
+                      int(bool(fast_diag)))
     res = nat.Result()
     up = lambda x: x.ctypes.data_as(C.POINTER(C.c_ubyte))  # noqa: E731
     st = nat.lib().rsylv_b200_solve_device(

@@ -284,6 +284,8 @@ struct Problem {
     // multi-rank: tile columns block-cyclic over nranks (column j owned by rank j % nranks).
     // Solved tiles are pushed into the peers' slots; peers are other GPUs (sys_scope = 1,
     // CUDA-IPC-mapped pointers) or virtual ranks sharing one GPU (sys_scope = 0).
+    int fast_solve;             // diagonal-tile solve: 0 = exact sub-block path (default),
+                                // 1 = fast plain-FP64 attempt first + exact fallback
     int nranks, rank, sys_scope;
     double* peerY[kMaxRanks];
     int* peerYexp[kMaxRanks];

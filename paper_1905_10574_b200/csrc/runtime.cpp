@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <functional>
 #include <map>
 #include <string>
@@ -246,6 +247,10 @@ int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std:
     P.x_omega = host_xf(PL.omega);
     P.x_target = host_xf(PL.omega * (1.0 - 0x1p-30));
     P.nranks = nranks;
+    {   // diagonal-tile solve path (RSYLV_B200_FAST_DIAG=1 opts in, for experiments)
+        const char* ev = std::getenv("RSYLV_B200_FAST_DIAG");
+        P.fast_solve = (A.opt.fast_diag || (ev && ev[0] == '1')) ? 1 : 0;
+    }
 
     PL.d_reason = nullptr;
     if (deferred) {

@@ -30,7 +30,7 @@ def rs():
     return m
 
 
-def gpu_solve(d, tile=None, scheduler=0, omega=None, probe=None):
+def gpu_solve(d, tile=None, scheduler=0, omega=None, probe=None, fast_diag=False):
     m = rs()
     A = m.QuasiTriangular.from_codes(d["a"], d["ab"] if d["ab"] is not None else
                                      np.ones(d["a"].shape[0], np.uint8))
@@ -40,7 +40,7 @@ def gpu_solve(d, tile=None, scheduler=0, omega=None, probe=None):
     cfg = m.OverflowConfig(omega=om if om > 0 else m.default_omega())
     try:
         r = m.solve_tiled_robust(A, B, d["c"], tile or d["tile"], cfg, scheduler=scheduler,
-                                 probe=probe)
+                                 probe=probe, fast_diag=fast_diag)
         return 0, r
     except m.ScaleUnderflowError as e:
         return 3, e.result
@@ -225,3 +225,38 @@ def test_nonfinite_input_rejected():
     A = m.QuasiTriangular(np.eye(6))
     with pytest.raises(ValueError):
         m.solve_tiled_robust(A, A, c, 3)
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_fast_diag_path_reference_suite(name):
+    """The opt-in fast diagonal-tile path (plain FP64 on the normalized tile, exact fallback)
+    against the reference with the same bars as the default path."""
+    d = CASES[name]
+    st, r = gpu_solve(d, fast_diag=True)
+    assert STATUS[st] == STATUS[d["status"]], (d["origin"], st)
+    if st == 0:
+        err = unscaled_ratio_err(r.y, r.alpha_exp, d["y"], d["alpha"])
+        assert err <= (1e-10 if name.startswith("twin") else 1e-12), (name, err)
+        om = d["omega"] if d["omega"] > 0 else WIDE / 2
+        assert r.max_tile_norm <= om
+    elif st == 2:
+        assert r.pivot == d["pivot"]
+
+
+@pytest.mark.parametrize("cfgname,n,t", [("c1", 400, 128), ("c1", 300, 64), ("c3", 96, 32),
+                                          ("c3", 128, 40)])
+def test_fast_diag_path_configs(cfgname, n, t):
+    """1x1-block tiles take the fast path; c3 growth overflows it and falls back."""
+    from paper_1905_10574_b200.configs import CONFIGS, host_system
+    cfg = CONFIGS[cfgname].scaled(n, tile=t)
+    a, ac, b, bc, c = host_system(cfg)
+    d = dict(a=a, ab=ac, b=b, bb=bc, c=c, tile=t, omega=0.0)
+    _, r0 = gpu_solve(d)
+    _, r1 = gpu_solve(d, fast_diag=True)
+    assert np.isfinite(r1.y).all()
+    if cfgname == "c3":
+        Y = bigrange.solve(a, ac, b, bc, c)
+        assert bigrange.rel_inf_diff_exp(r1.y, r1.alpha_exp, Y) <= 1e-12
+    else:
+        assert r0.alpha_exp == r1.alpha_exp == 0
+        assert golden.rel_inf_diff(r1.y, r0.y) <= 1e-13
