@@ -169,6 +169,26 @@ int rsylv_b200_debug_counters(unsigned long long* out32, int reset);
  * bit 1: force the exact solver); out256 (nullable) receives the solution, column-major. */
 int rsylv_b200_debug_subsolve(int reps, int mode, long long* cycles, double* out256);
 
+/* ---- FP64 GEMM and residual on the DMMA tensor path (device buffers, column-major) ----
+ * C = alpha * op(A) * op(B) + beta * C with op = transpose when ta / tb != 0 (op(A) m x k,
+ * op(B) k x n). a_upper: op(A) is upper quasi-triangular (zero below the first subdiagonal),
+ * b_upper: op(B) likewise -- the structural zeros are skipped. stream: cudaStream_t (NULL =
+ * legacy default stream). Used by the Bartels-Stewart transforms and the residual below. */
+int rsylv_b200_dgemm(rsylv_b200_ctx* ctx, int ta, int tb, size_t m, size_t n, size_t k,
+                     double alpha, const double* a, size_t lda, const double* b, size_t ldb,
+                     double beta, double* c, size_t ldc, int a_upper, int b_upper, void* stream);
+
+/* Relative residual of a solve (src/testgen.cpp:64-79, made overflow-safe):
+ *   || A Y + Y B - 2^alpha_exp C ||_F / ((||A||_F + ||B||_F) ||Y||_F + 2^alpha_exp ||C||_F)
+ * evaluated on the device in a power-of-two prescaled frame (Y * 2^s with max |Y * 2^s| <=
+ * 2^400), so that tiles near omega and alpha far below DBL_MIN stay representable. A (m x m)
+ * and B (n x n) are the dense upper quasi-triangular matrices. out[0] = relative residual,
+ * out[1..5] = ||R||, ||A||, ||B||, ||Y 2^s||, ||2^(alpha+s) C|| (Frobenius), out[6] = s. */
+int rsylv_b200_relative_residual(rsylv_b200_ctx* ctx, size_t m, size_t n, const double* a,
+                                 size_t lda, const double* b, size_t ldb, const double* c,
+                                 size_t ldc, const double* y, size_t ldy, int32_t alpha_exp,
+                                 void* stream, double* out7);
+
 /* ---- benchmark input generation (harness utility; not part of the reference API) ----
  * Fills a device buffer (column-major, ld) with a quasi-triangular matrix whose strict upper
  * triangle is U(up_lo, up_hi), 1x1 diagonal entries U(d_lo, d_hi) and 2x2 blocks

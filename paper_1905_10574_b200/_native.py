@@ -84,6 +84,12 @@ def lib():
         L.rsylv_b200_generate_rhs.argtypes = [_sz, _sz, C.c_void_p, _sz, C.c_uint64, C.c_int,
                                               C.c_double, C.c_double, C.POINTER(C.c_int32), _sz,
                                               _sz, C.c_double, C.c_void_p]
+        L.rsylv_b200_dgemm.argtypes = [C.c_void_p, C.c_int, C.c_int, _sz, _sz, _sz, C.c_double,
+                                       C.c_void_p, _sz, C.c_void_p, _sz, C.c_double, C.c_void_p,
+                                       _sz, C.c_int, C.c_int, C.c_void_p]
+        L.rsylv_b200_relative_residual.argtypes = [C.c_void_p, _sz, _sz, C.c_void_p, _sz,
+                                                   C.c_void_p, _sz, C.c_void_p, _sz, C.c_void_p,
+                                                   _sz, C.c_int32, C.c_void_p, _dp]
         _lib = L
     return _lib
 

@@ -304,3 +304,47 @@ def robust_update(c, c_exp: int, a, b, ab_exp: int, omega: float = 0.0, device: 
     if st != nat.RSYLV_OK:
         raise RuntimeError(f"robust_update failed: {st}")
     return c, int(ce.value), float(cn.value), int(ev.value)
+
+
+def _colmajor(t, name):
+    if t.stride(0) != 1:
+        raise ValueError(f"{name}: device arrays must be column-major (stride(0) == 1)")
+    return t.stride(1) if t.dim() == 2 and t.shape[1] > 1 else max(1, t.shape[0])
+
+
+def dgemm(a_dev, b_dev, c_dev, alpha: float = 1.0, beta: float = 0.0, ta: bool = False,
+          tb: bool = False, a_upper: bool = False, b_upper: bool = False, stream=None,
+          device: int = 0):
+    """C = alpha * op(A) op(B) + beta * C on the FP64 tensor path (rsylv_b200_dgemm), torch
+    CUDA tensors in column-major layout; a_upper / b_upper skip the structural zeros of an
+    upper quasi-triangular op(A) / op(B)."""
+    m, n = c_dev.shape
+    k = a_dev.shape[0] if ta else a_dev.shape[1]
+    if (b_dev.shape[1] if tb else b_dev.shape[0]) != k or (a_dev.shape[1] if ta else a_dev.shape[0]) != m \
+            or (b_dev.shape[0] if tb else b_dev.shape[1]) != n:
+        raise ValueError("dgemm: shapes do not conform")
+    st = nat.lib().rsylv_b200_dgemm(
+        nat.context(device), int(ta), int(tb), m, n, k, float(alpha), C.c_void_p(a_dev.data_ptr()),
+        _colmajor(a_dev, "A"), C.c_void_p(b_dev.data_ptr()), _colmajor(b_dev, "B"), float(beta),
+        C.c_void_p(c_dev.data_ptr()), _colmajor(c_dev, "C"), int(a_upper), int(b_upper),
+        C.c_void_p(stream) if stream is not None else None)
+    if st != nat.RSYLV_OK:
+        raise RuntimeError(f"rsylv_b200_dgemm: {nat.lib().rsylv_b200_status_string(st).decode()}")
+    return c_dev
+
+
+def relative_residual_device(a_dev, b_dev, c_dev, y_dev, alpha_exp: int, stream=None,
+                             device: int = 0) -> dict:
+    """Overflow-safe relative residual of A Y + Y B = 2^alpha_exp C on the device
+    (src/testgen.cpp:64-79 in a power-of-two prescaled frame; rsylv_b200_relative_residual)."""
+    m, n = c_dev.shape
+    out = (C.c_double * 7)()
+    st = nat.lib().rsylv_b200_relative_residual(
+        nat.context(device), m, n, C.c_void_p(a_dev.data_ptr()), _colmajor(a_dev, "A"),
+        C.c_void_p(b_dev.data_ptr()), _colmajor(b_dev, "B"), C.c_void_p(c_dev.data_ptr()),
+        _colmajor(c_dev, "C"), C.c_void_p(y_dev.data_ptr()), _colmajor(y_dev, "Y"),
+        int(alpha_exp), C.c_void_p(stream) if stream is not None else None, out)
+    if st != nat.RSYLV_OK:
+        raise RuntimeError(f"rsylv_b200_relative_residual: {nat.lib().rsylv_b200_status_string(st).decode()}")
+    return dict(relres=out[0], norm_r=out[1], norm_a=out[2], norm_b=out[3], norm_y=out[4],
+                norm_c=out[5], frame=int(out[6]))

@@ -33,6 +33,14 @@ void launch_persistent(const Problem& P, int grid, cudaStream_t st);
 cudaError_t launch_persistent_mr(const Problem* probs_dev, int nranks_here, int grid,
                                  cudaStream_t st);
 void launch_unpack(const Problem& P, int alpha_exp, double* y, long long ldy, cudaStream_t st);
+size_t smem_gemm();
+cudaError_t launch_dgemm(int ta, int tb, int m, int n, int k, double alpha, const double* A,
+                         long long lda, const double* B, long long ldb, double beta, double* C,
+                         long long ldc, int a_upper, int b_upper, cudaStream_t st);
+cudaError_t launch_scale_copy(int m, int n, const double* src, long long lds, double* dst,
+                              long long ldd, int e, cudaStream_t st);
+cudaError_t launch_absmax_sumsq(int m, int n, const double* x, long long ld, int e, int blocks,
+                                double* pmax, double* psum, cudaStream_t st);
 void launch_gen_qt(int n, double* a, long long ld, const unsigned char* blk,
                    unsigned long long seed, double up_lo, double up_hi, double d_lo, double d_hi,
                    double off_lo, double off_hi, cudaStream_t st);

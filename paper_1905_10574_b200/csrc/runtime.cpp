@@ -4,6 +4,7 @@
 // the TileGrid of tile_grid.cpp): argument validation in the reference's order, tile
 // partitioning, device workspace management, kernel launches (persistent dataflow scheduler or
 // host-driven wavefront), the alpha reduction (tile_grid.cpp:38-42) and the final verdict.
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <cstdio>
@@ -1049,6 +1050,101 @@ int rsylv_b200_robust_update(rsylv_b200_ctx* ctx, size_t m, size_t k, size_t n, 
 }
 
 // development: per-phase cycle counters of the tile tasks (reset=1 clears them)
+int rsylv_b200_dgemm(rsylv_b200_ctx* ctx, int ta, int tb, size_t m, size_t n, size_t k,
+                     double alpha, const double* a, size_t lda, const double* b, size_t ldb,
+                     double beta, double* c, size_t ldc, int a_upper, int b_upper, void* stream) {
+    if (!ctx || (m && n && k && (!a || !b)) || (m && n && !c)) return RSYLV_INVALID_ARGUMENT;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return RSYLV_CUDA_ERROR;
+    try {
+        ck(ctx, launch_dgemm(ta, tb, (int)m, (int)n, (int)k, alpha, a, (long long)lda, b,
+                             (long long)ldb, beta, c, (long long)ldc, a_upper, b_upper,
+                             as_stream(stream)), "dgemm");
+    } catch (const Fail& f) {
+        return f.status;
+    }
+    return RSYLV_OK;
+}
+
+namespace {
+// ||x||_F of an m x n column-major device matrix without overflow: max |x| first, then the sum
+// of squares of x * 2^-e(max). Returns the norm as (mantissa part, binary exponent).
+void frob_norm(rsylv_b200_ctx* ctx, const double* x, size_t m, size_t n, size_t ld,
+               cudaStream_t st, double* nm, int* ne) {
+    const int blocks = 2 * ctx->sms;
+    double* part = buf<double>(ctx, "res_part", 2 * (size_t)blocks);
+    std::vector<double> hm(blocks), hs(blocks);
+    ck(ctx, launch_absmax_sumsq((int)m, (int)n, x, (long long)ld, 0, blocks, part, part + blocks, st),
+       "absmax");
+    ck(ctx, cudaMemcpyAsync(hm.data(), part, sizeof(double) * blocks, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(ctx, cudaStreamSynchronize(st), "sync");
+    double mx = 0.0;
+    for (double v : hm) mx = (v != v || mx != mx) ? NAN : std::max(mx, v);
+    if (!(mx > 0.0) || std::isinf(mx)) {
+        *nm = mx;
+        *ne = 0;
+        return;
+    }
+    int e = 0;
+    std::frexp(mx, &e);
+    ck(ctx, launch_absmax_sumsq((int)m, (int)n, x, (long long)ld, -e, blocks, part, part + blocks, st),
+       "sumsq");
+    ck(ctx, cudaMemcpyAsync(hs.data(), part + blocks, sizeof(double) * blocks, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(ctx, cudaStreamSynchronize(st), "sync");
+    double s = 0.0;
+    for (double v : hs) s += v;
+    *nm = std::sqrt(s);
+    *ne = e;
+}
+}  // namespace
+
+int rsylv_b200_relative_residual(rsylv_b200_ctx* ctx, size_t m, size_t n, const double* a,
+                                 size_t lda, const double* b, size_t ldb, const double* c,
+                                 size_t ldc, const double* y, size_t ldy, int32_t alpha_exp,
+                                 void* stream, double* out7) {
+    if (!ctx || !out7 || m == 0 || n == 0) return RSYLV_INVALID_ARGUMENT;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return RSYLV_CUDA_ERROR;
+    try {
+        cudaStream_t st = as_stream(stream);
+        double ym;
+        int ye;
+        frob_norm(ctx, y, m, n, ldy, st, &ym, &ye);  // (only its max is needed: ye)
+        // the frame: Y * 2^s with max |Y 2^s| <= 2^400
+        const int s = ye > 400 ? 400 - ye : 0;
+        double* Ys = buf<double>(ctx, "res_ys", m * n);
+        double* R = buf<double>(ctx, "res_r", m * n);
+        ck(ctx, launch_scale_copy((int)m, (int)n, y, (long long)ldy, Ys, (long long)m, s, st), "scale");
+        ck(ctx, launch_scale_copy((int)m, (int)n, c, (long long)ldc, R, (long long)m, alpha_exp + s, st),
+           "scale");
+        double rn, an, bn, yn, cn;
+        int re, ae, be, yse, ce;
+        frob_norm(ctx, R, m, n, m, st, &cn, &ce);
+        // R = A Ys - R, then R += Ys B (triangular K ranges skipped)
+        ck(ctx, launch_dgemm(0, 0, (int)m, (int)n, (int)m, 1.0, a, (long long)lda, Ys, (long long)m,
+                             -1.0, R, (long long)m, 1, 0, st), "dgemm");
+        ck(ctx, launch_dgemm(0, 0, (int)m, (int)n, (int)n, 1.0, Ys, (long long)m, b, (long long)ldb,
+                             1.0, R, (long long)m, 0, 1, st), "dgemm");
+        frob_norm(ctx, R, m, n, m, st, &rn, &re);
+        frob_norm(ctx, a, m, m, lda, st, &an, &ae);
+        frob_norm(ctx, b, n, n, ldb, st, &bn, &be);
+        frob_norm(ctx, Ys, m, n, m, st, &yn, &yse);
+        auto val = [](double v, int e) { return std::ldexp(v, e); };
+        // denominator in the common frame 2^yse (||A||, ||B|| are moderate: tile norms <= omega)
+        const double ab = val(an, ae) + val(bn, be);
+        const int top = std::max({yse + 0, ce, re});
+        const double den = ab * val(yn, yse - top) + val(cn, ce - top);
+        out7[0] = val(rn, re - top) / den;
+        out7[1] = val(rn, re);
+        out7[2] = val(an, ae);
+        out7[3] = val(bn, be);
+        out7[4] = val(yn, yse);
+        out7[5] = val(cn, ce);
+        out7[6] = s;
+    } catch (const Fail& f) {
+        return f.status;
+    }
+    return RSYLV_OK;
+}
+
 int rsylv_b200_debug_counters(unsigned long long* out32, int reset) {
     if (reset) return reset_prof() == cudaSuccess ? RSYLV_OK : RSYLV_CUDA_ERROR;
     return read_prof(out32) == cudaSuccess ? RSYLV_OK : RSYLV_CUDA_ERROR;
