@@ -14,8 +14,9 @@ Inputs are 12.8 GB per matrix, far larger than the 126 MB L2, so no L2 flush is 
            HOST buffers: H2D of A, B, C and D2H of Y inside the timed region.
 * roofline: the tile-DAG kernel (DMMA update GEMMs + diagonal solves) against the measured
            FP64 DMMA peak of this pool's B200 (profiles/r01_fp64_peak_probe.log).
-* cpu_baseline: the UNMODIFIED reference (oracle/_ref/librsylv_ref.so, built from
-           /root/reference sources) on a bounded sample on this host's cores.
+* cpu_baseline: the UNMODIFIED reference (oracle/_ref/librsylv_ref[_v4].so, built from
+           /root/reference sources) on this host's cores: c1 at its literal size, the larger
+           configs on a bounded sample, at the reference's best tile size.
 
 --impl reference runs only the reference CPU path (rank 0) on that sample and prints its line.
 Multi-GPU (N > 1): one process per GPU (torchrun); tile columns block-cyclic over the ranks, solved
@@ -109,32 +110,55 @@ class ClockSampler:
 
 
 def cpu_sample_cfg(cfg):
-    """Bounded CPU sample of the workload: the same distributions, hot tiles included, at
-    CPU_SAMPLE^2 with the config's tile size. For c5 that is 1280^2, tile 512, one C tile
-    x 1e250: the reference completes it WITH robust scaling (alpha = 3.3e-20), whereas the
-    literal 40000^2 system (and 1536^2, 2048^2) ends in ScaleUnderflowError."""
+    """Bounded CPU sample of the workload. c1 (2000^2), the one config the reference solves, is
+    run at its literal size (same_config). The others use the same distributions, hot tiles
+    included, at CPU_SAMPLE^2: for c5 that is 1280^2 with one C tile x 1e250, which the
+    reference completes WITH robust scaling (alpha = 3.3e-20), whereas the literal 40000^2
+    system (and 1536^2, 2048^2 with this seed) ends in ScaleUnderflowError."""
+    if cfg.m * cfg.n <= 2000 * 2000:
+        return cfg
     s = min(CPU_SAMPLE, cfg.m, cfg.n)
     return cfg.scaled(s, s)
 
 
-def run_cpu_reference(cfg, reps: int):
-    """Times the unmodified reference rsylv::solve_tiled_robust (parallel mode, all cores)."""
+def run_cpu_reference(cfg, reps: int, seq: bool = False):
+    """Times the unmodified reference rsylv::solve_tiled_robust (parallel mode, all host cores;
+    the x86-64-v4 / AVX-512 build when the host has it, as the reference's -march=native build
+    would) on the bounded sample, at the reference's best tile size among {128, 256, the
+    config's}: its tile solve is super-cubic in the tile size, so the
+    config's 512 would understate it. Returns the sample, the chosen tile, the step times
+    at that tile and a description."""
+    os.environ.setdefault("RSYLV_REF_VARIANT", "native")
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as po
     from paper_1905_10574_b200.configs import host_system
     scfg = cpu_sample_cfg(cfg)
     a, ac, b, bc, c = host_system(scfg)
     cores = os.cpu_count() or 1
-    times, status = [], None
-    for _ in range(reps):
+    per_tile = {}
+    for t in sorted({128, 256, scfg.tile}):
         t0 = time.perf_counter()
-        r = po.solve_tiled(a, ac, b, bc, c, scfg.tile, impl="ref", workers=cores)
+        r = po.solve_tiled(a, ac, b, bc, c, t, impl="ref", workers=cores)
+        per_tile[t] = (time.perf_counter() - t0, r.status)
+    best = min(per_tile, key=lambda t: per_tile[t][0])
+    times, status = [], per_tile[best][1]
+    for _ in range(max(0, reps - 1)):
+        t0 = time.perf_counter()
+        r = po.solve_tiled(a, ac, b, bc, c, best, impl="ref", workers=cores)
         times.append(time.perf_counter() - t0)
         status = r.status
-    sample = (f"reference rsylv::solve_tiled_robust, parallel({cores}), {scfg.m}x{scfg.n} tile "
-              f"{scfg.tile}, {cfg.name} distributions (hot tiles included); status "
-              f"{po.STATUS_NAMES[status]}")
-    return scfg, times, cores, sample
+    times = [per_tile[best][0]] + times
+    extra = {"tiles_s": {str(t): round(v[0], 4) for t, v in per_tile.items()},
+             "build": f"x86-64-{po.ref_variant()}", "same_config": scfg is cfg}
+    if seq:
+        t0 = time.perf_counter()
+        po.solve_tiled(a, ac, b, bc, c, best, impl="ref", workers=0)
+        extra["sequential_s"] = round(time.perf_counter() - t0, 4)
+        extra["sequential_gflops"] = scfg.flops() / extra["sequential_s"] / 1e9
+    sample = (f"reference rsylv::solve_tiled_robust, parallel({cores}), {scfg.m}x{scfg.n} at its "
+              f"best tile {best} (of {sorted(per_tile)}), {cfg.name} distributions (hot tiles "
+              f"included), {extra['build']} build; status {po.STATUS_NAMES[status]}")
+    return scfg, best, times, cores, sample, extra
 
 
 def reference_arm(args):
@@ -143,7 +167,8 @@ def reference_arm(args):
     cfg = CONFIGS[args.config]
     if rank != 0:
         return
-    scfg, times, cores, sample = run_cpu_reference(cfg, args.warmup + args.steps)
+    scfg, best, times, cores, sample, extra = run_cpu_reference(
+        cfg, args.warmup + args.steps, seq=scfg_is_small(cfg))
     timed = times[args.warmup:] or times
     t = sum(timed)
     val = scfg.flops() * len(timed) / t / 1e9
@@ -152,12 +177,19 @@ def reference_arm(args):
             "warmup": args.warmup, "ms_per_step": 1e3 * t / len(timed), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{cfg.name}: {cfg.note}", "sample": f"{scfg.m}x{scfg.n}",
-                       "tile": scfg.tile},
+                       "tile": best, "config_tile": cfg.tile,
+                       "same_config": extra["same_config"]},
             "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": cores,
-                             "kind": "reference", "sample": sample},
+                             "kind": "reference", "sample": sample, **extra},
             "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def scfg_is_small(cfg) -> bool:
+    """Configs the reference completes at their literal size in seconds (c1): also timed in
+    sequential() mode."""
+    return cfg.m * cfg.n <= 2000 * 2000
 
 
 def _free_port() -> int:
@@ -329,9 +361,9 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        scfg, times, cores, sample = run_cpu_reference(cfg, 1)
+        scfg, best, times, cores, sample, extra = run_cpu_reference(cfg, 1, seq=scfg_is_small(cfg))
         cpu = {"value": scfg.flops() / times[0] / 1e9, "unit": "GFLOP/s", "cores": cores,
-               "kind": "reference", "sample": sample}
+               "kind": "reference", "sample": sample, **extra}
 
     # DRAM traffic of the dominant kernel per launch, from the committed ncu capture of the same
     # command (ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum -k k_persistent)

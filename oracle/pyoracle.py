@@ -48,10 +48,29 @@ _REF = None
 _ORA = None
 
 
+def host_has_avx512() -> bool:
+    try:
+        with open("/proc/cpuinfo") as f:
+            flags = f.read()
+        return all(x in flags for x in ("avx512f", "avx512bw", "avx512dq", "avx512vl", "avx512cd"))
+    except OSError:
+        return False
+
+
+def ref_variant() -> str:
+    """Which reference build ref_lib() loads: "v3" (x86-64-v3, the pinned test build) unless
+    RSYLV_REF_VARIANT=native asks for the best build this host runs (x86-64-v4 / AVX-512 when
+    available: the CPU baseline of bench.py, mirroring the reference's -march=native)."""
+    want = os.environ.get("RSYLV_REF_VARIANT", "v3")
+    if want == "native" and host_has_avx512() and os.path.exists(os.path.join(REF_DIR, "librsylv_ref_v4.so")):
+        return "v4"
+    return "v3"
+
+
 def ref_lib():
     global _REF
     if _REF is None:
-        lib = _lib("librsylv_ref.so")
+        lib = _lib("librsylv_ref_v4.so" if ref_variant() == "v4" else "librsylv_ref.so")
         lib.ref_solve_tiled.argtypes = [_sz, _sz, _dp, _sz, _up, _dp, _sz, _up, _dp, _sz, _sz,
                                         C.c_double, C.c_double, _sz, _dp, _sz, _dp, _u64p, _dp]
         lib.ref_solve_robust_scalar.argtypes = [_sz, _sz, _dp, _up, _dp, _up, _dp, C.c_double,

@@ -2,9 +2,10 @@
 
 Solves the general real Sylvester equation A X + X B = α C (A m×m, B n×n, no structure) by
     A = U Ã Uᵀ, B = V B̃ Vᵀ          real Schur forms
-    C̃ = Uᵀ C V                      two GEMMs on the GPU (cuBLAS DGEMM via torch)
+    C̃ = Uᵀ C V                      two GEMMs on the GPU (this package's FP64 DMMA GEMM,
+                                    rsylv_b200_dgemm)
     Ã Y + Y B̃ = α C̃                 the robust tiled solve (this package's CUDA engine)
-    X = U Y Vᵀ                      two GEMMs on the GPU
+    X = U Y Vᵀ                      two GEMMs on the GPU (rsylv_b200_dgemm)
 The reference solves only the triangular inner problem; this is the wrapper a
 user of the full equation needs. The Schur factorizations run on the host (LAPACK dgees via
 scipy): there is no GPU real-Schur routine in this image, and they are preprocessing outside the
@@ -49,17 +50,23 @@ def solve_sylvester(a, b, c, tile_size: int = 128, cfg: Optional[api.OverflowCon
     tb = np.triu(tb, -1)
     qa, qb = api.QuasiTriangular(ta), api.QuasiTriangular(tb)
     dev = torch.device("cuda", device)
-    U = torch.as_tensor(ua, device=dev)
-    V = torch.as_tensor(ub, device=dev)
-    Ct = (U.T @ torch.as_tensor(c, device=dev) @ V)
-    # the device entry takes column-major tensors
-    cm = lambda x: x.T.contiguous().T  # noqa: E731
-    A_d, B_d = cm(torch.as_tensor(qa.matrix(), device=dev)), cm(torch.as_tensor(qb.matrix(), device=dev))
-    C_d = cm(Ct)
-    Y_d = torch.empty((n, m), dtype=torch.float64, device=dev).T
+    # every device matrix is column-major (the C-ABI layout)
+    cm = lambda x: torch.as_tensor(np.asfortranarray(x), device=dev).T.contiguous().T  # noqa: E731
+    empty = lambda r, k: torch.empty((k, r), dtype=torch.float64, device=dev).T  # noqa: E731
+    U, V, Cd = cm(ua), cm(ub), cm(c)
+    T = empty(m, n)
+    api.dgemm(U, Cd, T, ta=True, device=device)            # T = Uᵀ C
+    C_d = empty(m, n)
+    api.dgemm(T, V, C_d, device=device)                    # C̃ = T V
+    A_d, B_d = cm(qa.matrix()), cm(qb.matrix())
+    Y_d = empty(m, n)
     st, res = api.solve_tiled_robust_device(A_d, qa.codes, B_d, qb.codes, C_d, Y_d, tile_size,
                                             cfg, device=device, raise_underflow=False)
-    X = (U @ Y_d @ V.T).cpu().numpy()
+    api.dgemm(U, Y_d, T, device=device)                    # T = U Y
+    X_d = empty(m, n)
+    api.dgemm(T, V, X_d, tb=True, device=device)           # X = T Vᵀ
+    torch.cuda.synchronize(dev)
+    X = X_d.cpu().numpy()
     return X, int(res.alpha_exp)
 
 
