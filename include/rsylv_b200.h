@@ -131,6 +131,19 @@ int rsylv_b200_solve_device(rsylv_b200_ctx* ctx, size_t m, size_t n, const doubl
                             size_t ldy, const rsylv_b200_options* opt, void* stream,
                             rsylv_b200_result* res);
 
+/* ---- multi-GPU in one process (the drop-in path for ExecutionMode::workers > 1): R contexts on
+ * R distinct GPUs (rsylv_b200_create per device), HOST buffers as rsylv_b200_solve. Tile columns
+ * block-cyclic over the GPUs (column j on ctxs[j % R]); each GPU stores the upper tiles of A and B
+ * and its own tile columns of C; solved tiles are pushed to the peers over NVLink (peer
+ * access), alpha is the MIN over the GPUs. R = 1 is rsylv_b200_solve on ctxs[0]. */
+int rsylv_b200_solve_group(rsylv_b200_ctx* const* ctxs, int R, size_t m, size_t n,
+                           const double* a, size_t lda, const unsigned char* ablk, const double* b,
+                           size_t ldb, const unsigned char* bblk, const double* c, size_t ldc,
+                           double* y, size_t ldy, const rsylv_b200_options* opt,
+                           rsylv_b200_result* res);
+/* Visible CUDA devices (0 when none / the driver is unusable). */
+int rsylv_b200_device_count(void);
+
 /* ---- multi-GPU (one process per GPU; tile columns block-cyclic, column j on rank j % nranks).
  * Sequence per solve (the caller provides the collectives, e.g. torch.distributed):
  *   1. rsylv_b200_dist_prepare  : partition, allocate, pack, validate; writes this rank's IPC
@@ -168,6 +181,23 @@ int rsylv_b200_debug_counters(unsigned long long* out32, int reset);
 /* Development: average cycles of one warp-level 16x16 sub-block solve (mode bit 0: 2x2 blocks,
  * bit 1: force the exact solver); out256 (nullable) receives the solution, column-major. */
 int rsylv_b200_debug_subsolve(int reps, int mode, long long* cycles, double* out256);
+
+/* Development / test entries for the pieces of the diagonal-tile solver (HOST buffers):
+ * rsylv_b200_debug_small_solve: n independent 1x1 / 2x1 / 1x2 / 2x2 block Sylvester solves
+ *   a_t z + z b_t = c_t (rs[t], cs[t] in {1, 2}; a, b, c, z 2x2 column-major per case) with the
+ *   exact path's complete-pivoting Kronecker solve and division guard (small_solve.cpp:15-106):
+ *   on return A z + z B = 2^-dz[t] c, status[t] 0 ok / 2 singular (pivot[t]).
+ * rsylv_b200_debug_guards: the exponent-form guards for n inputs -- update guard of
+ *   (c + a b) (ProtectUpdate, overflow.cpp:15-40) in the xq integer form (update-phase source
+ *   headers) and the xf form (in-tile updates), division guard of bnd / |t| (ProtectDivision,
+ *   overflow.cpp:48-64; -1 for t = 0). Each returns d: the scale factor is 2^-d. */
+int rsylv_b200_debug_small_solve(size_t n, const int32_t* rs, const int32_t* cs, const double* a,
+                                 const double* b, const double* c, double omega,
+                                 double small_num, double* z, int32_t* dz, int32_t* status,
+                                 double* pivot);
+int rsylv_b200_debug_guards(size_t n, const double* c, const double* a, const double* b,
+                            const double* bnd, const double* t, double omega, int32_t* d_upd_xq,
+                            int32_t* d_upd_xf, int32_t* d_div);
 
 /* ---- FP64 GEMM and residual on the DMMA tensor path (device buffers, column-major) ----
  * C = alpha * op(A) * op(B) + beta * C with op = transpose when ta / tb != 0 (op(A) m x k,

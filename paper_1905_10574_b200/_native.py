@@ -90,6 +90,15 @@ def lib():
         L.rsylv_b200_relative_residual.argtypes = [C.c_void_p, _sz, _sz, C.c_void_p, _sz,
                                                    C.c_void_p, _sz, C.c_void_p, _sz, C.c_void_p,
                                                    _sz, C.c_int32, C.c_void_p, _dp]
+        L.rsylv_b200_solve_group.argtypes = [C.POINTER(C.c_void_p), C.c_int, _sz, _sz, _dp, _sz,
+                                             _up, _dp, _sz, _up, _dp, _sz, _dp, _sz,
+                                             C.POINTER(Options), C.POINTER(Result)]
+        L.rsylv_b200_device_count.argtypes = []
+        _ip = C.POINTER(C.c_int32)
+        L.rsylv_b200_debug_small_solve.argtypes = [_sz, _ip, _ip, _dp, _dp, _dp, C.c_double,
+                                                   C.c_double, _dp, _ip, _ip, _dp]
+        L.rsylv_b200_debug_guards.argtypes = [_sz, _dp, _dp, _dp, _dp, _dp, C.c_double, _ip, _ip,
+                                              _ip]
         _lib = L
     return _lib
 

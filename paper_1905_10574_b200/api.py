@@ -16,6 +16,7 @@ Everything runs on the CUDA extension; there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Sequence
 
@@ -209,9 +210,11 @@ def solve_tiled_robust(a: QuasiTriangular, b: QuasiTriangular, c, tile_size: int
     """Solves A*Y + Y*B = alpha*C with every tile of Y bounded by cfg.omega (tiled_solve.hpp:29-40).
 
     HOST arrays in, HOST array out (the reference calling convention). ``mode.workers`` is the
-    reference's worker count; a single GPU serves every value (multi-GPU runs go through
-    bench.py / torchrun). ``host_pipeline`` (0 auto, 1 on, -1 off) streams the inputs to the
-    device tile column by tile column while the solve runs (rsylv_b200_options)."""
+    reference's worker count and maps to GPUs like the C++ shim: w >= 2 solves on min(w, visible
+    GPUs, 8) GPUs of this process (rsylv_b200_solve_group); with one visible GPU and
+    RSYLV_B200_VIRTUAL_RANKS=1, min(w, 8) virtual ranks share it (a probe keeps one GPU).
+    ``host_pipeline`` (0 auto, 1 on, -1 off) streams the inputs to the device tile column by tile
+    column while the solve runs (rsylv_b200_options)."""
     cfg = cfg or OverflowConfig()
     c = np.asarray(c, dtype=np.float64)
     if c.ndim != 2 or c.shape[0] != a.dim() or c.shape[1] != b.dim():
@@ -230,8 +233,20 @@ def solve_tiled_robust(a: QuasiTriangular, b: QuasiTriangular, c, tile_size: int
     dp = lambda x: x.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
     up = lambda x: x.ctypes.data_as(C.POINTER(C.c_ubyte))  # noqa: E731
     am, bm = a.matrix(), b.matrix()
-    st = nat.lib().rsylv_b200_solve(nat.context(device), m, n, dp(am), m, up(a.codes), dp(bm), n,
-                                    up(b.codes), dp(cf), m, dp(y), m, C.byref(opt), C.byref(res))
+    w = min(int(mode.workers), 8) if mode is not None else 0
+    gpus = nat.lib().rsylv_b200_device_count() if (w >= 2 and probe is None) else 1
+    if w >= 2 and probe is None and gpus >= 2:
+        R = min(w, gpus)
+        ctxs = (C.c_void_p * R)(*[nat.context(d) for d in range(R)])
+        st = nat.lib().rsylv_b200_solve_group(ctxs, R, m, n, dp(am), m, up(a.codes), dp(bm), n,
+                                              up(b.codes), dp(cf), m, dp(y), m, C.byref(opt),
+                                              C.byref(res))
+    else:
+        if w >= 2 and probe is None and os.environ.get("RSYLV_B200_VIRTUAL_RANKS") == "1":
+            opt.virtual_ranks = w
+        st = nat.lib().rsylv_b200_solve(nat.context(device), m, n, dp(am), m, up(a.codes), dp(bm),
+                                        n, up(b.codes), dp(cf), m, dp(y), m, C.byref(opt),
+                                        C.byref(res))
     cfg.scaling_events += int(res.scaling_events)
     _replay_probe(res, pbuf, probe)
     out = SolveResult(res.alpha, y, int(res.alpha_exp), int(res.scaling_events), res.device_ms,
@@ -348,3 +363,52 @@ def relative_residual_device(a_dev, b_dev, c_dev, y_dev, alpha_exp: int, stream=
         raise RuntimeError(f"rsylv_b200_relative_residual: {nat.lib().rsylv_b200_status_string(st).decode()}")
     return dict(relres=out[0], norm_r=out[1], norm_a=out[2], norm_b=out[3], norm_y=out[4],
                 norm_c=out[5], frame=int(out[6]))
+
+
+def _dptr(x):
+    return x.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _iptr(x):
+    return x.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def debug_small_solve(cases, omega: float = 0.0, small_num: float = 0.0, device: int = 0):
+    """The diagonal-tile solver's exact block solve (complete pivoting + division guard) on
+    single blocks: cases = [(a, b, c)] with a rs x rs, b cs x cs, c rs x cs (rs, cs in {1, 2}).
+    Returns [(status, z, dz, pivot)] with a z + z b = 2^-dz c (rsylv_b200_debug_small_solve)."""
+    nat.context(device)
+    n = len(cases)
+    rs = np.array([np.shape(a)[0] for a, _, _ in cases], dtype=np.int32)
+    cs = np.array([np.shape(b)[0] for _, b, _ in cases], dtype=np.int32)
+    pack = lambda xs: np.stack([np.pad(np.asarray(x, float).reshape(np.shape(x)),  # noqa: E731
+                                       ((0, 2 - np.shape(x)[0]), (0, 2 - np.shape(x)[1])))
+                                .flatten(order="F") for x in xs])
+    A, B, Cm = pack([a for a, _, _ in cases]), pack([b for _, b, _ in cases]), pack([c for _, _, c in cases])
+    Z = np.zeros((n, 4))
+    dz, stt = np.zeros(n, np.int32), np.zeros(n, np.int32)
+    piv = np.zeros(n)
+    st = nat.lib().rsylv_b200_debug_small_solve(n, _iptr(rs), _iptr(cs), _dptr(A), _dptr(B),
+                                                _dptr(Cm), float(omega), float(small_num),
+                                                _dptr(Z), _iptr(dz), _iptr(stt), _dptr(piv))
+    if st != nat.RSYLV_OK:
+        raise RuntimeError("rsylv_b200_debug_small_solve failed")
+    out = []
+    for t in range(n):
+        z = Z[t].reshape((2, 2), order="F")[:rs[t], :cs[t]]
+        out.append((int(stt[t]), z, int(dz[t]), float(piv[t])))
+    return out
+
+
+def debug_guards(c, a, b, bnd, t, omega: float, device: int = 0):
+    """Exponent-form guards (rsylv_b200_debug_guards): returns (d_update_xq, d_update_xf,
+    d_division) arrays; the scale factor is 2^-d (-1: division by zero)."""
+    nat.context(device)
+    arrs = [np.ascontiguousarray(x, dtype=np.float64) for x in (c, a, b, bnd, t)]
+    n = len(arrs[0])
+    o = [np.zeros(n, np.int32) for _ in range(3)]
+    st = nat.lib().rsylv_b200_debug_guards(n, *[_dptr(x) for x in arrs], float(omega),
+                                           *[_iptr(x) for x in o])
+    if st != nat.RSYLV_OK:
+        raise RuntimeError("rsylv_b200_debug_guards failed")
+    return tuple(o)

@@ -34,6 +34,12 @@ cudaError_t launch_persistent_mr(const Problem* probs_dev, int nranks_here, int 
                                  cudaStream_t st);
 void launch_unpack(const Problem& P, int alpha_exp, double* y, long long ldy, cudaStream_t st);
 size_t smem_gemm();
+void launch_debug_small(int n, const int* rs, const int* cs, const double* a, const double* b,
+                        const double* c, double omega, double small_num, double* z, int* dz,
+                        int* st, double* piv);
+void launch_debug_guards(int n, const double* c, const double* a, const double* b,
+                         const double* bnd, const double* t, double omega, int* dxq, int* dxf,
+                         int* ddiv);
 cudaError_t launch_dgemm(int ta, int tb, int m, int n, int k, double alpha, const double* A,
                          long long lda, const double* B, long long ldb, double beta, double* C,
                          long long ldc, int a_upper, int b_upper, cudaStream_t st);

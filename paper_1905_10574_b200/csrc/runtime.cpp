@@ -147,6 +147,7 @@ struct rsylv_b200_plan_holder {
     Plan plan;
     std::vector<std::vector<unsigned char>> peer_handles;  // opened handle bytes per peer
     std::vector<void*> peer_ptrs;                          // 5 per peer
+    bool raw_peers = false;  // peer_ptrs are plain device pointers (single-process multi-GPU)
 };
 
 namespace {
@@ -159,10 +160,12 @@ Plan& ctx_plan(rsylv_b200_ctx* ctx) { return ctx_holder(ctx).plan; }
 
 void close_peers(rsylv_b200_ctx* ctx) {
     rsylv_b200_plan_holder& H = ctx_holder(ctx);
-    for (void* p : H.peer_ptrs)
-        if (p) cudaIpcCloseMemHandle(p);
+    if (!H.raw_peers)
+        for (void* p : H.peer_ptrs)
+            if (p) cudaIpcCloseMemHandle(p);
     H.peer_ptrs.clear();
     H.peer_handles.clear();
+    H.raw_peers = false;
 }
 
 // Steps shared by every mode: partition (tile cut moved earlier around 2x2 blocks), device
@@ -291,6 +294,7 @@ int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std:
         ck(ctx, cudaMemsetAsync(B.ev, 0, 2 * sizeof(unsigned long long), st), "memset");
         ck(ctx, cudaMemsetAsync(B.tnext, 0, sizeof(int), st), "memset");
         Problem Q = P;
+        Q.rank = r;  // (multi-rank: C packed for the owned tile columns only)
         Q.Ypack = B.Yp;
         Q.ynorm = B.ynorm;
         Q.yexp = B.yexp;
@@ -326,7 +330,14 @@ int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std:
     std::vector<double> h_an((size_t)M * M), h_bn((size_t)N * N), h_yn(ny);
     ck(ctx, cudaMemcpyAsync(h_an.data(), anorm, sizeof(double) * M * M, cudaMemcpyDeviceToHost, st), "d2h");
     ck(ctx, cudaMemcpyAsync(h_bn.data(), bnorm, sizeof(double) * N * N, cudaMemcpyDeviceToHost, st), "d2h");
-    ck(ctx, cudaMemcpyAsync(h_yn.data(), PL.rb[0].ynorm, sizeof(double) * ny, cudaMemcpyDeviceToHost, st), "d2h");
+    // C tile norms: every local rank packed its owned tile columns (multi-rank)
+    for (size_t li = 0; li < local.size(); ++li) {
+        std::vector<double> part(ny);
+        ck(ctx, cudaMemcpyAsync(part.data(), PL.rb[li].ynorm, sizeof(double) * ny, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(ctx, cudaStreamSynchronize(st), "sync");
+        for (size_t t = 0; t < ny; ++t)
+            if (nranks == 1 || (int)(t % N) % nranks == local[li]) h_yn[t] = part[t];
+    }
     ck(ctx, cudaStreamSynchronize(st), "sync");
     for (int i = 0; i < M; ++i)
         for (int k = i; k < M; ++k)
@@ -340,7 +351,7 @@ int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std:
                 res->invalid_reason = RSYLV_REASON_B_BOUND;
                 return RSYLV_INVALID_ARGUMENT;
             }
-    for (size_t t = 0; t < ny; ++t)
+    for (size_t t = 0; t < ny; ++t)  // (one rank per process: its owned columns; together all)
         if (!(h_yn[t] <= PL.omega)) {
             res->invalid_reason = RSYLV_REASON_C_BOUND;
             return RSYLV_INVALID_ARGUMENT;
@@ -378,6 +389,10 @@ Problem rank_problem(rsylv_b200_ctx* ctx, size_t li) {
         Q.probe_cap = PL.probe_cap;  // every launch of the solve (main and side streams) logs
     }
     if (PL.nranks > 1) {
+        // RSYLV_B200_SYS_SCOPE=1 (tests): system-scope flags and fences also for virtual ranks,
+        // so the multi-GPU acquire / release code runs on one device
+        const char* ss = std::getenv("RSYLV_B200_SYS_SCOPE");
+        if (ss && ss[0] == '1') Q.sys_scope = 1;
         if (PL.local.size() > 1) {  // virtual ranks on this device
             for (size_t lj = 0; lj < PL.local.size(); ++lj) {
                 const RankBufs& O = PL.rb[lj];
@@ -410,12 +425,14 @@ Problem rank_problem(rsylv_b200_ctx* ctx, size_t li) {
 // pack + validation work (and the remaining DAG CTAs) on the side stream, which the main
 // stream joins before the alpha reduction
 constexpr int kPipeReserve = 4;
-int plan_run(rsylv_b200_ctx* ctx, rsylv_b200_result* res, int* emin_out, double* numax_out,
-             const std::function<void()>* side = nullptr) {
+// plan_launch enqueues the tile DAG (asynchronous); plan_collect waits for it and reduces.
+// plan_run = both. A single-process multi-GPU solve launches every device first, then collects
+// (a device's kernel waits on tiles its peers produce).
+int plan_launch(rsylv_b200_ctx* ctx, rsylv_b200_result* res,
+                const std::function<void()>* side = nullptr) {
     Plan& PL = ctx_plan(ctx);
     cudaStream_t st = PL.st;
     const int M = PL.M, N = PL.N;
-    const size_t ny = PL.ny;
     ck(ctx, cudaEventRecord(ctx->evp, st), "event");
     if (PL.nranks == 1) {
         Problem P = rank_problem(ctx, 0);
@@ -462,6 +479,18 @@ int plan_run(rsylv_b200_ctx* ctx, rsylv_b200_result* res, int* emin_out, double*
         res->dag_launches = 1;
     }
     ck(ctx, cudaEventRecord(ctx->evd, st), "event");
+    return RSYLV_OK;
+}
+
+// pivot_owned (optional): set when a singular failure's pivot was read from a tile this
+// context owns (multi-GPU: the owner's pivot is the one to report)
+int plan_collect(rsylv_b200_ctx* ctx, rsylv_b200_result* res, int* emin_out, double* numax_out,
+                 bool* pivot_owned = nullptr) {
+    Plan& PL = ctx_plan(ctx);
+    cudaStream_t st = PL.st;
+    const int M = PL.M, N = PL.N;
+    const size_t ny = PL.ny;
+    if (pivot_owned) *pivot_owned = false;
 
     // ---- alpha reduction (tile_grid.cpp:38-42) over the owned tiles, exponent form
     std::vector<int> ye_all(ny, 0);
@@ -497,9 +526,11 @@ int plan_run(rsylv_b200_ctx* ctx, rsylv_b200_result* res, int* emin_out, double*
                 best_enc = h_err[1];
                 const int pri = 0x7fffffff - h_err[1];
                 const int k = M - 1 - pri / N, l = pri % N;
-                if ((l % PL.nranks) == PL.local[li])
+                if ((l % PL.nranks) == PL.local[li]) {
                     ck(ctx, cudaMemcpy(&piv, B.tpiv + (size_t)k * N + l, sizeof(double),
                                        cudaMemcpyDeviceToHost), "d2h");
+                    if (pivot_owned) *pivot_owned = true;
+                }
             }
             if (!first_err) first_err = h_err[0];
         } else if (h_err[0] != 0 && (!first_err || first_err == kErrSingular)) {
@@ -531,6 +562,13 @@ int plan_run(rsylv_b200_ctx* ctx, rsylv_b200_result* res, int* emin_out, double*
     *emin_out = emin;
     *numax_out = numax_rel;
     return RSYLV_OK;
+}
+
+int plan_run(rsylv_b200_ctx* ctx, rsylv_b200_result* res, int* emin_out, double* numax_out,
+             const std::function<void()>* side = nullptr) {
+    const int st = plan_launch(ctx, res, side);
+    if (st != RSYLV_OK) return st;
+    return plan_collect(ctx, res, emin_out, numax_out);
 }
 
 // Largest s >= 0 with numax * 2^s <= omega and emin + s <= 0 (joint renormalisation).
@@ -605,6 +643,64 @@ int guarded_call(rsylv_b200_ctx* ctx, int (*fn)(rsylv_b200_ctx*, const SolveArgs
     }
 }
 
+}  // namespace
+
+namespace {
+// host <-> device staging for the debug entries (plain cudaMalloc / cudaMemcpy, synchronous)
+struct Staging {
+    std::vector<void*> ptrs;
+    bool ok = true;
+    template <class T>
+    T* up(const T* h, size_t n) {
+        void* d = nullptr;
+        if (cudaMalloc(&d, sizeof(T) * (n ? n : 1)) != cudaSuccess) {
+            ok = false;
+            return nullptr;
+        }
+        ptrs.push_back(d);
+        if (h && n && cudaMemcpy(d, h, sizeof(T) * n, cudaMemcpyHostToDevice) != cudaSuccess) ok = false;
+        return static_cast<T*>(d);
+    }
+    template <class T>
+    void down(T* h, const T* d, size_t n) {
+        if (ok && n && cudaMemcpy(h, d, sizeof(T) * n, cudaMemcpyDeviceToHost) != cudaSuccess) ok = false;
+    }
+    ~Staging() {
+        for (void* p : ptrs) cudaFree(p);
+    }
+};
+}  // namespace
+
+namespace {
+// ||x||_F of an m x n column-major device matrix without overflow: max |x| first, then the sum
+// of squares of x * 2^-e(max). Returns the norm as (mantissa part, binary exponent).
+void frob_norm(rsylv_b200_ctx* ctx, const double* x, size_t m, size_t n, size_t ld,
+               cudaStream_t st, double* nm, int* ne) {
+    const int blocks = 2 * ctx->sms;
+    double* part = buf<double>(ctx, "res_part", 2 * (size_t)blocks);
+    std::vector<double> hm(blocks), hs(blocks);
+    ck(ctx, launch_absmax_sumsq((int)m, (int)n, x, (long long)ld, 0, blocks, part, part + blocks, st),
+       "absmax");
+    ck(ctx, cudaMemcpyAsync(hm.data(), part, sizeof(double) * blocks, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(ctx, cudaStreamSynchronize(st), "sync");
+    double mx = 0.0;
+    for (double v : hm) mx = (v != v || mx != mx) ? NAN : std::max(mx, v);
+    if (!(mx > 0.0) || std::isinf(mx)) {
+        *nm = mx;
+        *ne = 0;
+        return;
+    }
+    int e = 0;
+    std::frexp(mx, &e);
+    ck(ctx, launch_absmax_sumsq((int)m, (int)n, x, (long long)ld, -e, blocks, part, part + blocks, st),
+       "sumsq");
+    ck(ctx, cudaMemcpyAsync(hs.data(), part + blocks, sizeof(double) * blocks, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(ctx, cudaStreamSynchronize(st), "sync");
+    double s = 0.0;
+    for (double v : hs) s += v;
+    *nm = std::sqrt(s);
+    *ne = e;
+}
 }  // namespace
 
 extern "C" {
@@ -839,6 +935,187 @@ int rsylv_b200_solve(rsylv_b200_ctx* ctx, size_t m, size_t n, const double* a, s
     return guarded_call(ctx, solve_host_impl, A);
 }
 
+// Single-process multi-GPU solve on HOST buffers: one context per GPU (distinct devices), tile
+// columns block-cyclic over them (column j on ctxs[j % R]). Every GPU gets the upper tiles of A
+// and B (replicated: any tile row may need any A_ik) and only its owned tile columns of C; Y is
+// copied back per owned column. Solved tiles are pushed to the peers over NVLink through plain
+// peer pointers (cudaDeviceEnablePeerAccess; the multi-process form uses CUDA IPC), the alpha
+// reduction is the host-side MIN over the contexts, then each GPU rescales and copies out its
+// columns. The reference's parallel API maps here (ExecutionMode::workers -> GPUs, the shim).
+int rsylv_b200_solve_group(rsylv_b200_ctx* const* ctxs, int R, size_t m, size_t n,
+                           const double* a, size_t lda, const unsigned char* ablk, const double* b,
+                           size_t ldb, const unsigned char* bblk, const double* c, size_t ldc,
+                           double* y, size_t ldy, const rsylv_b200_options* opt,
+                           rsylv_b200_result* res) {
+    if (!ctxs || R < 1 || R > kMaxRanks || !opt || !res) return RSYLV_INVALID_ARGUMENT;
+    for (int r = 0; r < R; ++r)
+        if (!ctxs[r]) return RSYLV_INVALID_ARGUMENT;
+    if (R == 1) return rsylv_b200_solve(ctxs[0], m, n, a, lda, ablk, b, ldb, bblk, c, ldc, y, ldy, opt, res);
+    for (int r = 0; r < R; ++r)
+        for (int q = r + 1; q < R; ++q)
+            if (ctxs[r]->device == ctxs[q]->device) return RSYLV_INVALID_ARGUMENT;  // distinct GPUs
+    init_result(res);
+    if (opt->tile_size < 2) {
+        res->invalid_reason = RSYLV_REASON_TILE_SIZE;
+        return RSYLV_INVALID_ARGUMENT;
+    }
+    if (m == 0 || n == 0) {
+        res->alpha = 1.0;
+        return RSYLV_OK;
+    }
+    rsylv_b200_ctx* failed = ctxs[0];
+    try {
+        const size_t ts = std::min<size_t>(opt->tile_size, (size_t)kTileMax);
+        std::vector<unsigned char> acodes = codes_or_ones(ablk, m), bcodes = codes_or_ones(bblk, n);
+        const std::vector<int> rcut = partition(acodes.data(), m, ts);
+        const std::vector<int> ccut = partition(bcodes.data(), n, ts);
+        const int N = (int)ccut.size() - 1;
+        std::vector<rsylv_b200_result> rr(R);
+        std::vector<double*> dy(R);
+        unsigned long long h2d = 0, d2h = 0;
+        // 1. per GPU: upper tiles of A and B, owned tile columns of C; plan + pack + validate
+        for (int r = 0; r < R; ++r) {
+            rsylv_b200_ctx* ctx = ctxs[r];
+            failed = ctx;
+            ck(ctx, cudaSetDevice(ctx->device), "device");
+            cudaStream_t st = ctx->own_stream;
+            double* da = buf<double>(ctx, "hA", m * m);
+            double* db = buf<double>(ctx, "hB", n * n);
+            double* dc = buf<double>(ctx, "hC", m * n);
+            dy[r] = buf<double>(ctx, "hY", m * n);
+            for (size_t k = 0; k + 1 < rcut.size(); ++k) {
+                const size_t c0 = rcut[k], c1 = rcut[k + 1];
+                ck(ctx, cudaMemcpy2DAsync(da + c0 * m, m * 8, a + c0 * lda, lda * 8, c1 * 8, c1 - c0,
+                                          cudaMemcpyHostToDevice, st), "h2d A");
+                h2d += 8ull * c1 * (c1 - c0);
+            }
+            for (int j = 0; j < N; ++j) {
+                const size_t c0 = ccut[j], c1 = ccut[j + 1];
+                ck(ctx, cudaMemcpy2DAsync(db + c0 * n, n * 8, b + c0 * ldb, ldb * 8, c1 * 8, c1 - c0,
+                                          cudaMemcpyHostToDevice, st), "h2d B");
+                h2d += 8ull * c1 * (c1 - c0);
+                if (j % R != r) continue;
+                ck(ctx, cudaMemcpy2DAsync(dc + c0 * m, m * 8, c + c0 * ldc, ldc * 8, m * 8, c1 - c0,
+                                          cudaMemcpyHostToDevice, st), "h2d C");
+                h2d += 8ull * m * (c1 - c0);
+            }
+            SolveArgs D{m, n, da, db, dc, m, n, m, ablk, bblk, dy[r], m, *opt, st, &rr[r]};
+            D.opt.scheduler = 0;
+            init_result(&rr[r]);
+            const int sp = plan_prepare(ctx, D, R, std::vector<int>{r});
+            if (sp != RSYLV_OK) {
+                res->invalid_reason = rr[r].invalid_reason;
+                return sp;
+            }
+        }
+        // 2. peer access + the peers' workspace pointers
+        for (int r = 0; r < R; ++r) {
+            failed = ctxs[r];
+            ck(ctxs[r], cudaSetDevice(ctxs[r]->device), "device");
+            for (int q = 0; q < R; ++q) {
+                if (q == r) continue;
+                int can = 0;
+                ck(ctxs[r], cudaDeviceCanAccessPeer(&can, ctxs[r]->device, ctxs[q]->device), "peer query");
+                if (!can) {
+                    ctxs[r]->last_error = "no peer access between the GPUs of the group";
+                    return RSYLV_CUDA_ERROR;
+                }
+                const cudaError_t e = cudaDeviceEnablePeerAccess(ctxs[q]->device, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled)
+                    (void)cudaGetLastError();
+                else
+                    ck(ctxs[r], e, "enable peer access");
+            }
+            close_peers(ctxs[r]);
+            rsylv_b200_plan_holder& H = ctx_holder(ctxs[r]);
+            H.peer_ptrs.assign(5 * R, nullptr);
+            H.peer_handles.assign(R, {});
+            H.raw_peers = true;
+            for (int q = 0; q < R; ++q) {
+                if (q == r) continue;
+                const RankBufs& Bq = ctx_plan(ctxs[q]).rb[0];
+                void* ptrs[5] = {Bq.Yp, Bq.yexp, Bq.ynorm, Bq.state, Bq.err};
+                for (int k = 0; k < 5; ++k) H.peer_ptrs[5 * q + k] = ptrs[k];
+            }
+        }
+        // 3. launch every GPU's tile DAG, then 4. collect (a GPU waits on its peers' tiles)
+        for (int r = 0; r < R; ++r) {
+            failed = ctxs[r];
+            ck(ctxs[r], cudaSetDevice(ctxs[r]->device), "device");
+            const int sl = plan_launch(ctxs[r], &rr[r]);
+            if (sl != RSYLV_OK) return sl;
+        }
+        int emin = 0, status = RSYLV_OK;
+        double numax = 0.0, pivot = 0.0;
+        std::vector<int> em(R);
+        std::vector<double> nu(R);
+        unsigned long long events = 0;
+        for (int r = 0; r < R; ++r) {
+            failed = ctxs[r];
+            ck(ctxs[r], cudaSetDevice(ctxs[r]->device), "device");
+            bool owned = false;
+            const int sc = plan_collect(ctxs[r], &rr[r], &em[r], &nu[r], &owned);
+            events += rr[r].scaling_events;
+            if (sc != RSYLV_OK) {
+                if (status == RSYLV_OK || status == RSYLV_SINGULAR) {
+                    if (sc == RSYLV_SINGULAR) {
+                        if (owned || status == RSYLV_OK) pivot = rr[r].pivot;
+                    }
+                    status = (status == RSYLV_OK || sc != RSYLV_SINGULAR) ? sc : status;
+                }
+                continue;
+            }
+            emin = std::min(emin, em[r]);
+        }
+        res->scaling_events = events;
+        res->row_tiles = rr[0].row_tiles;
+        res->col_tiles = rr[0].col_tiles;
+        if (status != RSYLV_OK) {
+            res->pivot = pivot;
+            return status;
+        }
+        for (int r = 0; r < R; ++r) numax = std::max(numax, std::ldexp(nu[r], emin - em[r]));
+        const int ae = alpha_exponent(emin, numax, ctx_plan(ctxs[0]).omega);
+        // 5. consistency scaling + copy-out of the owned columns
+        int fin = RSYLV_OK;
+        double dev_ms = 0.0;
+        for (int r = 0; r < R; ++r) {
+            rsylv_b200_ctx* ctx = ctxs[r];
+            failed = ctx;
+            ck(ctx, cudaSetDevice(ctx->device), "device");
+            fin = plan_finish(ctx, ae, numax, emin, dy[r], m, &rr[r]);
+            dev_ms = std::max(dev_ms, rr[r].device_ms);
+            for (int j = r; j < N; j += R) {
+                const size_t c0 = ccut[j], c1 = ccut[j + 1];
+                ck(ctx, cudaMemcpy2DAsync(y + c0 * ldy, ldy * 8, dy[r] + c0 * m, m * 8, m * 8, c1 - c0,
+                                          cudaMemcpyDeviceToHost, ctx->own_stream), "d2h Y");
+                d2h += 8ull * m * (c1 - c0);
+            }
+        }
+        for (int r = 0; r < R; ++r) ck(ctxs[r], cudaStreamSynchronize(ctxs[r]->own_stream), "sync");
+        res->alpha_exp = ae;
+        res->alpha = rr[0].alpha;
+        res->max_tile_norm = rr[0].max_tile_norm;
+        res->device_ms = dev_ms;
+        res->dag_launches = R;
+        res->h2d_bytes = h2d;
+        res->d2h_bytes = d2h;
+        return fin;
+    } catch (const Fail& f) {
+        (void)failed;
+        return f.status;
+    }
+}
+
+int rsylv_b200_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
 int rsylv_b200_dist_prepare(rsylv_b200_ctx* ctx, int nranks, int rank, size_t m, size_t n,
                             const double* a, size_t lda, const unsigned char* ablk,
                             const double* b, size_t ldb, const unsigned char* bblk,
@@ -1065,38 +1342,6 @@ int rsylv_b200_dgemm(rsylv_b200_ctx* ctx, int ta, int tb, size_t m, size_t n, si
     return RSYLV_OK;
 }
 
-namespace {
-// ||x||_F of an m x n column-major device matrix without overflow: max |x| first, then the sum
-// of squares of x * 2^-e(max). Returns the norm as (mantissa part, binary exponent).
-void frob_norm(rsylv_b200_ctx* ctx, const double* x, size_t m, size_t n, size_t ld,
-               cudaStream_t st, double* nm, int* ne) {
-    const int blocks = 2 * ctx->sms;
-    double* part = buf<double>(ctx, "res_part", 2 * (size_t)blocks);
-    std::vector<double> hm(blocks), hs(blocks);
-    ck(ctx, launch_absmax_sumsq((int)m, (int)n, x, (long long)ld, 0, blocks, part, part + blocks, st),
-       "absmax");
-    ck(ctx, cudaMemcpyAsync(hm.data(), part, sizeof(double) * blocks, cudaMemcpyDeviceToHost, st), "d2h");
-    ck(ctx, cudaStreamSynchronize(st), "sync");
-    double mx = 0.0;
-    for (double v : hm) mx = (v != v || mx != mx) ? NAN : std::max(mx, v);
-    if (!(mx > 0.0) || std::isinf(mx)) {
-        *nm = mx;
-        *ne = 0;
-        return;
-    }
-    int e = 0;
-    std::frexp(mx, &e);
-    ck(ctx, launch_absmax_sumsq((int)m, (int)n, x, (long long)ld, -e, blocks, part, part + blocks, st),
-       "sumsq");
-    ck(ctx, cudaMemcpyAsync(hs.data(), part + blocks, sizeof(double) * blocks, cudaMemcpyDeviceToHost, st), "d2h");
-    ck(ctx, cudaStreamSynchronize(st), "sync");
-    double s = 0.0;
-    for (double v : hs) s += v;
-    *nm = std::sqrt(s);
-    *ne = e;
-}
-}  // namespace
-
 int rsylv_b200_relative_residual(rsylv_b200_ctx* ctx, size_t m, size_t n, const double* a,
                                  size_t lda, const double* b, size_t ldb, const double* c,
                                  size_t ldc, const double* y, size_t ldy, int32_t alpha_exp,
@@ -1143,6 +1388,53 @@ int rsylv_b200_relative_residual(rsylv_b200_ctx* ctx, size_t m, size_t n, const 
         return f.status;
     }
     return RSYLV_OK;
+}
+
+int rsylv_b200_debug_small_solve(size_t n, const int32_t* rs, const int32_t* cs, const double* a,
+                                 const double* b, const double* c, double omega,
+                                 double small_num, double* z, int32_t* dz, int32_t* status,
+                                 double* pivot) {
+    if (n == 0) return RSYLV_OK;
+    if (!rs || !cs || !a || !b || !c || !z || !dz || !status || !pivot) return RSYLV_INVALID_ARGUMENT;
+    for (size_t t = 0; t < n; ++t)
+        if (rs[t] < 1 || rs[t] > 2 || cs[t] < 1 || cs[t] > 2) return RSYLV_INVALID_ARGUMENT;
+    Staging S;
+    const int* drs = S.up(rs, n);
+    const int* dcs = S.up(cs, n);
+    const double* da = S.up(a, 4 * n);
+    const double* db = S.up(b, 4 * n);
+    const double* dc = S.up(c, 4 * n);
+    double* dzv = S.up<double>(nullptr, 4 * n);
+    int* ddz = S.up<int>(nullptr, n);
+    int* dst = S.up<int>(nullptr, n);
+    double* dpv = S.up<double>(nullptr, n);
+    if (!S.ok) return RSYLV_CUDA_ERROR;
+    launch_debug_small((int)n, drs, dcs, da, db, dc, omega > 0 ? omega : DBL_MAX / 2,
+                       small_num > 0 ? small_num : DBL_MIN / DBL_EPSILON, dzv, ddz, dst, dpv);
+    if (cudaGetLastError() != cudaSuccess) return RSYLV_CUDA_ERROR;
+    S.down(z, dzv, 4 * n);
+    S.down(dz, ddz, n);
+    S.down(status, dst, n);
+    S.down(pivot, dpv, n);
+    return S.ok ? RSYLV_OK : RSYLV_CUDA_ERROR;
+}
+
+int rsylv_b200_debug_guards(size_t n, const double* c, const double* a, const double* b,
+                            const double* bnd, const double* t, double omega, int32_t* d_upd_xq,
+                            int32_t* d_upd_xf, int32_t* d_div) {
+    if (n == 0) return RSYLV_OK;
+    if (!c || !a || !b || !bnd || !t || !d_upd_xq || !d_upd_xf || !d_div) return RSYLV_INVALID_ARGUMENT;
+    Staging S;
+    const double *dc = S.up(c, n), *da = S.up(a, n), *db = S.up(b, n), *dbn = S.up(bnd, n),
+                 *dt = S.up(t, n);
+    int *o1 = S.up<int>(nullptr, n), *o2 = S.up<int>(nullptr, n), *o3 = S.up<int>(nullptr, n);
+    if (!S.ok) return RSYLV_CUDA_ERROR;
+    launch_debug_guards((int)n, dc, da, db, dbn, dt, omega, o1, o2, o3);
+    if (cudaGetLastError() != cudaSuccess) return RSYLV_CUDA_ERROR;
+    S.down(d_upd_xq, o1, n);
+    S.down(d_upd_xf, o2, n);
+    S.down(d_div, o3, n);
+    return S.ok ? RSYLV_OK : RSYLV_CUDA_ERROR;
 }
 
 int rsylv_b200_debug_counters(unsigned long long* out32, int reset) {

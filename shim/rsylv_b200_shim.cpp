@@ -16,10 +16,17 @@
 //  * SingularEquationError(pivot), ScaleUnderflowError as in errors.hpp;
 //  * OverflowConfig::scaling_events is bumped by the device's guard-activation count (the
 //    granularity differs from the CPU solver: compare trends only);
-//  * ExecutionMode::workers is accepted and ignored (one GPU serves every worker count);
+//  * ExecutionMode::workers (tiled_solve.hpp:16-22) maps to GPUs:
+//    workers <= 1 -> one GPU; workers = w >= 2 -> min(w, visible GPUs, 8) GPUs of this process
+//    (rsylv_b200_solve_group: tile columns block-cyclic, solved tiles pushed over NVLink). With a
+//    single visible GPU and RSYLV_B200_VIRTUAL_RANKS=1 in the environment, min(w, 8) virtual
+//    ranks share that GPU instead (the same exchange, used by the tests); a TileProbe request
+//    keeps the solve on one GPU (the probe log is per GPU);
 //  * TileProbe is replayed after the solve from the device's probe log, tile indices of the
 //    B200 partition (tiles <= 128, cut moved earlier around 2x2 blocks).
+#include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cmath>
 #include <mutex>
 #include <stdexcept>
@@ -34,6 +41,7 @@ namespace {
 
 std::mutex g_mu;
 rsylv_b200_ctx* g_ctx = nullptr;
+std::vector<rsylv_b200_ctx*> g_group;  // one context per GPU for workers >= 2
 
 rsylv_b200_ctx* context() {
     if (!g_ctx) {
@@ -43,6 +51,24 @@ rsylv_b200_ctx* context() {
                                      rsylv_b200_status_string(st) + ")");
     }
     return g_ctx;
+}
+
+// contexts of GPUs 0 .. R-1 (context 0 is the single-GPU one when it lives on device 0)
+const std::vector<rsylv_b200_ctx*>& group(int R) {
+    while ((int)g_group.size() < R) {
+        const int d = (int)g_group.size();
+        rsylv_b200_ctx* c = nullptr;
+        const int st = rsylv_b200_create(d, &c);
+        if (st != RSYLV_OK)
+            throw std::runtime_error(std::string("rsylv-b200: cannot open GPU ") + std::to_string(d));
+        g_group.push_back(c);
+    }
+    return g_group;
+}
+
+bool env_on(const char* name) {
+    const char* v = std::getenv(name);
+    return v && v[0] == '1';
 }
 
 std::vector<unsigned char> codes(const rsylv::QuasiTriangular& q) {
@@ -59,7 +85,6 @@ SolveResult solve_tiled_robust(const QuasiTriangular& a, const QuasiTriangular& 
                                ConstMatrixView c, std::size_t tile_size,
                                const OverflowConfig& cfg, ExecutionMode mode,
                                const TileProbe& probe) {
-    (void)mode;
     if (c.rows != a.dim() || c.cols != b.dim())
         throw std::invalid_argument("solve_tiled_robust: C does not conform with A and B");
     if (tile_size < 2) throw std::invalid_argument("partition: requested tile size must be >= 2");
@@ -80,9 +105,19 @@ SolveResult solve_tiled_robust(const QuasiTriangular& a, const QuasiTriangular& 
     int st;
     {
         std::lock_guard<std::mutex> hold(g_mu);
-        st = rsylv_b200_solve(context(), m, n, a.matrix().data(), m, ac.data(),
-                              b.matrix().data(), n, bc.data(), c.data, c.ld, out.y.data(), m,
-                              &opt, &res);
+        const int w = (int)std::min<std::size_t>(mode.workers, 8);
+        const int gpus = w >= 2 && !probe ? rsylv_b200_device_count() : 1;
+        if (w >= 2 && !probe && gpus >= 2) {
+            const int R = std::min(w, gpus);
+            st = rsylv_b200_solve_group(group(R).data(), R, m, n, a.matrix().data(), m, ac.data(),
+                                        b.matrix().data(), n, bc.data(), c.data, c.ld,
+                                        out.y.data(), m, &opt, &res);
+        } else {
+            if (w >= 2 && !probe && env_on("RSYLV_B200_VIRTUAL_RANKS")) opt.virtual_ranks = w;
+            st = rsylv_b200_solve(context(), m, n, a.matrix().data(), m, ac.data(),
+                                  b.matrix().data(), n, bc.data(), c.data, c.ld, out.y.data(), m,
+                                  &opt, &res);
+        }
     }
     if (cfg.scaling_events) cfg.scaling_events->fetch_add(res.scaling_events, std::memory_order_relaxed);
     if (probe) {
@@ -111,7 +146,7 @@ SolveResult solve_tiled_robust(const QuasiTriangular& a, const QuasiTriangular& 
             throw ScaleUnderflowError();
         default:
             throw std::runtime_error(std::string("rsylv-b200: ") + rsylv_b200_status_string(st) +
-                                     ": " + rsylv_b200_last_error(g_ctx));
+                                     ": " + rsylv_b200_last_error(g_ctx ? g_ctx : g_group.front()));
     }
 }
 

@@ -2,6 +2,12 @@
 compiled from /root/reference by shim/Makefile) relinked with shim/rsylv_b200_shim.cpp in place of
 src/tiled_solve.cpp, i.e. every rsylv::solve_tiled_robust call runs on the GPU.
 
+ExecutionMode::workers maps to GPUs in the shim. The second run sets RSYLV_B200_VIRTUAL_RANKS=1,
+so on a one-GPU box criterion 5 ("parallel consistency", workers 2/4/8,
+acceptance_main.cpp:213-236) compares 2-, 4- and 8-rank solves (tile columns block-cyclic,
+solved tiles pushed between rank workspaces) with the sequential one -- not one GPU against
+itself.
+
 Expected verdicts (profiles/r01/acceptance_b200.log):
   1, 2, 5, 7, 8 PASS (the reference itself fails 7: it aborts on ScaleUnderflowError);
   3 FAIL exactly like the reference (no representable alpha exists at m=n=200, omega=1e4);
@@ -20,8 +26,15 @@ BIN = os.path.join(ROOT, "oracle", "_ref", "acceptance_b200")
 
 
 @pytest.mark.skipif(not os.path.exists(BIN), reason="acceptance_b200 not built (needs /root/reference)")
-def test_reference_acceptance_suite_through_shim():
-    out = subprocess.run([BIN], capture_output=True, text=True, timeout=900).stdout
+@pytest.mark.parametrize("virtual", [False, True])
+def test_reference_acceptance_suite_through_shim(virtual):
+    env = dict(os.environ)
+    if virtual:
+        env["RSYLV_B200_VIRTUAL_RANKS"] = "1"
+    out = subprocess.run([BIN], capture_output=True, text=True, timeout=900, env=env).stdout
+    if virtual and os.path.isdir(os.path.join(ROOT, "gpurun_out")):
+        with open(os.path.join(ROOT, "gpurun_out", "acceptance_b200_virtual_ranks.log"), "w") as f:
+            f.write(out)
     verdict = {}
     for line in out.splitlines():
         m = re.match(r"\[(PASS|FAIL|REPORT)\] criterion (\d+):", line)

@@ -59,3 +59,65 @@ def test_virtual_ranks_larger_system():
         mant, ex = np.frexp(ref.alpha)
         got = np.ldexp(r1.y * mant, int(ex) - r1.alpha_exp)
         assert golden.rel_inf_diff(got, ref.y) <= 1e-10
+
+
+@pytest.mark.parametrize("name", ["growth_n100_t25", "twin_c5_192x192_t64", "singular_n8"])
+def test_virtual_ranks_with_system_scope(name, monkeypatch):
+    """RSYLV_B200_SYS_SCOPE=1: the one-rank-per-GPU memory model (ld.acquire.sys /
+    st.release.sys flags, __threadfence_system before every push and publish, system-scope
+    atomics on the peers' error words) on virtual ranks of one GPU -- the device code of the
+    multi-GPU push path, bitwise equal to the single-rank solve."""
+    monkeypatch.setenv("RSYLV_B200_SYS_SCOPE", "1")
+    d = CASES[name]
+    s1, r1 = solve(d, 1)
+    for R in (2, 4):
+        sR, rR = solve(d, R)
+        assert s1 == sR
+        if s1 == 2:
+            assert rR.pivot == r1.pivot
+            continue
+        assert r1.alpha_exp == rR.alpha_exp and np.array_equal(r1.y, rR.y)
+
+
+@pytest.mark.parametrize("w", [2, 4, 8])
+def test_execution_mode_workers_map_to_ranks(w, monkeypatch):
+    """ExecutionMode::parallel(w) (tiled_solve.hpp:16-22) reaches the multi-GPU path: with one
+    visible GPU and RSYLV_B200_VIRTUAL_RANKS=1 it runs min(w, 8) virtual ranks; results are
+    bitwise those of sequential() (acceptance criterion 5, acceptance_main.cpp:213-236)."""
+    import paper_1905_10574_b200 as m
+    monkeypatch.setenv("RSYLV_B200_VIRTUAL_RANKS", "1")
+    d = CASES["twin_c2_160x160_t32"]
+    A = m.QuasiTriangular.from_codes(d["a"], d["ab"])
+    B = m.QuasiTriangular.from_codes(d["b"], d["bb"])
+    r0 = m.solve_tiled_robust(A, B, d["c"], 32, mode=m.ExecutionMode.sequential())
+    rw = m.solve_tiled_robust(A, B, d["c"], 32, mode=m.ExecutionMode.parallel(w))
+    assert r0.alpha_exp == rw.alpha_exp and np.array_equal(r0.y, rw.y)
+
+
+def test_group_solve_api_contract():
+    """rsylv_b200_solve_group: R = 1 is the single-GPU solve; contexts must be distinct GPUs."""
+    import ctypes as C
+    import paper_1905_10574_b200 as m
+    from paper_1905_10574_b200 import _native as nat
+    d = CASES["twin_c2_160x160_t32"]
+    A = m.QuasiTriangular.from_codes(d["a"], d["ab"])
+    B = m.QuasiTriangular.from_codes(d["b"], d["bb"])
+    ref = m.solve_tiled_robust(A, B, d["c"], 32)
+    mm, nn = d["c"].shape
+    cf = np.asfortranarray(d["c"])
+    y = np.zeros((mm, nn), order="F")
+    opt = nat.Options(m.default_omega(), m.default_small_num(), 32, 0, 0, 0, 0)
+    res = nat.Result()
+    dp = lambda x: x.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+    up = lambda x: x.ctypes.data_as(C.POINTER(C.c_ubyte))  # noqa: E731
+    am, bm = A.matrix(), B.matrix()
+    L = nat.lib()
+    one = (C.c_void_p * 1)(nat.context(0))
+    st = L.rsylv_b200_solve_group(one, 1, mm, nn, dp(am), mm, up(A.codes), dp(bm), nn,
+                                  up(B.codes), dp(cf), mm, dp(y), mm, C.byref(opt), C.byref(res))
+    assert st == nat.RSYLV_OK and res.alpha_exp == ref.alpha_exp and np.array_equal(y, ref.y)
+    two = (C.c_void_p * 2)(nat.context(0), nat.context(0))
+    st = L.rsylv_b200_solve_group(two, 2, mm, nn, dp(am), mm, up(A.codes), dp(bm), nn,
+                                  up(B.codes), dp(cf), mm, dp(y), mm, C.byref(opt), C.byref(res))
+    assert st == nat.RSYLV_INVALID_ARGUMENT
+    assert L.rsylv_b200_device_count() >= 1
