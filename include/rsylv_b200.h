@@ -141,6 +141,9 @@ int rsylv_b200_solve_group(rsylv_b200_ctx* const* ctxs, int R, size_t m, size_t 
                            size_t ldb, const unsigned char* bblk, const double* c, size_t ldc,
                            double* y, size_t ldy, const rsylv_b200_options* opt,
                            rsylv_b200_result* res);
+/* 1 when the opt-in fast diagonal-tile path (rsylv_b200_options.fast_diag) is compiled in
+ * (make EXTRA=-DRSYLV_FAST_DIAG_BUILD=1); otherwise fast_diag requests run the exact path. */
+int rsylv_b200_has_fast_diag(void);
 /* Visible CUDA devices (0 when none / the driver is unusable). */
 int rsylv_b200_device_count(void);
 

@@ -94,6 +94,7 @@ def lib():
                                              _up, _dp, _sz, _up, _dp, _sz, _dp, _sz,
                                              C.POINTER(Options), C.POINTER(Result)]
         L.rsylv_b200_device_count.argtypes = []
+        L.rsylv_b200_has_fast_diag.argtypes = []
         _ip = C.POINTER(C.c_int32)
         L.rsylv_b200_debug_small_solve.argtypes = [_sz, _ip, _ip, _dp, _dp, _dp, C.c_double,
                                                    C.c_double, _dp, _ip, _ip, _dp]

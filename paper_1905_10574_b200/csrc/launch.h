@@ -8,6 +8,7 @@
 namespace rsb {
 
 size_t smem_task();
+int has_fast_diag();
 int bench_subsolve(int reps, int mode, long long* cycles_host, double* out256);
 cudaError_t read_prof(unsigned long long* out);
 cudaError_t reset_prof();

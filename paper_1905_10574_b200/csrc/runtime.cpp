@@ -1107,6 +1107,8 @@ int rsylv_b200_solve_group(rsylv_b200_ctx* const* ctxs, int R, size_t m, size_t 
     }
 }
 
+int rsylv_b200_has_fast_diag(void) { return has_fast_diag(); }
+
 int rsylv_b200_device_count(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) {

@@ -227,6 +227,16 @@ def test_nonfinite_input_rejected():
         m.solve_tiled_robust(A, A, c, 3)
 
 
+def _fast_built():
+    from paper_1905_10574_b200 import _native as nat
+    return nat.lib().rsylv_b200_has_fast_diag() == 1
+
+
+fast_only = pytest.mark.skipif("not _fast_built()", reason="fast diagonal path not compiled in "
+                               "(make EXTRA=-DRSYLV_FAST_DIAG_BUILD=1)")
+
+
+@fast_only
 @pytest.mark.parametrize("name", sorted(CASES))
 def test_fast_diag_path_reference_suite(name):
     """The opt-in fast diagonal-tile path (plain FP64 on the normalized tile, exact fallback)
@@ -243,6 +253,7 @@ def test_fast_diag_path_reference_suite(name):
         assert r.pivot == d["pivot"]
 
 
+@fast_only
 @pytest.mark.parametrize("cfgname,n,t", [("c1", 400, 128), ("c1", 300, 64), ("c3", 96, 32),
                                           ("c3", 128, 40)])
 def test_fast_diag_path_configs(cfgname, n, t):
