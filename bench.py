@@ -427,8 +427,9 @@ def main():
     # DRAM traffic of the dominant kernel per launch, from the committed ncu capture of the same
     # command (ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum -k k_persistent)
     traffic, traffic_src = None, None
-    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01",
-                         f"traffic_{cfg.name}_k_persistent.csv")
+    here = os.path.dirname(os.path.abspath(__file__))
+    tpath = next((p for p in (os.path.join(here, "profiles", r, f"traffic_{cfg.name}_k_persistent.csv")
+                              for r in ("r02", "r01")) if os.path.exists(p)), "")
     if os.path.exists(tpath) and args.scheduler == 0 and world == 1:
         import csv
         vals = {}

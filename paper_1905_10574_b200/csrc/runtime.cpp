@@ -863,7 +863,45 @@ static int solve_host_pipelined(rsylv_b200_ctx* ctx, const SolveArgs& H, double*
     return status;
 }
 
+// Page-locks the caller's host buffers for the duration of one rsylv_b200_solve (the reference's
+// DenseMatrix storage is ordinary pageable memory): cudaMemcpy*Async from pageable memory is
+// staged and blocks the host thread, which would serialize the host pipeline's per-column
+// copies ahead of the DAG launch instead of overlapping them with it. Buffers that are already
+// pinned / registered, or smaller than 64 MB, are left alone; RSYLV_B200_HOST_REGISTER=0 turns
+// it off.
+struct HostRegistration {
+    std::vector<void*> regs;
+    bool enabled = true;
+    HostRegistration() {
+        const char* e = std::getenv("RSYLV_B200_HOST_REGISTER");
+        enabled = !(e && e[0] == '0');
+    }
+    void add(const void* p, size_t bytes, bool read_only) {
+        if (!enabled || !p || bytes < ((size_t)64 << 20)) return;
+        cudaPointerAttributes at;
+        if (cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type != cudaMemoryTypeUnregistered)
+            return;
+        (void)cudaGetLastError();
+        const unsigned fl = cudaHostRegisterDefault | (read_only ? cudaHostRegisterReadOnly : 0);
+        if (cudaHostRegister(const_cast<void*>(p), bytes, fl) == cudaSuccess)
+            regs.push_back(const_cast<void*>(p));
+        else
+            (void)cudaGetLastError();  // (overlapping ranges, limits: the plain path still works)
+    }
+    ~HostRegistration() {
+        for (void* p : regs) cudaHostUnregister(p);
+    }
+};
+
 static int solve_host_impl(rsylv_b200_ctx* ctx, const SolveArgs& H) {
+    HostRegistration reg;
+    const auto span = [](size_t rows, size_t cols, size_t ld) {
+        return cols ? ((cols - 1) * ld + rows) * sizeof(double) : 0;
+    };
+    reg.add(H.a, span(H.m, H.m, H.lda), true);
+    reg.add(H.b, span(H.n, H.n, H.ldb), true);
+    reg.add(H.c, span(H.m, H.n, H.ldc), true);
+    reg.add(H.y, span(H.m, H.n, H.ldy), false);
     cudaStream_t st = H.st;
     const size_t m = H.m, n = H.n;
     double* da = buf<double>(ctx, "hA", m * m);

@@ -135,3 +135,21 @@ print(r.alpha_exp)
     assert int(p.stdout.split()[-1]) == r.alpha_exp
     assert np.array_equal(np.load(out), r.y)
     os.remove(out)
+
+
+def test_pageable_buffers_page_locked_for_the_call(monkeypatch):
+    """The reference's DenseMatrix storage is pageable: rsylv_b200_solve page-locks buffers of
+    >= 64 MB for the call (so the host pipeline's per-column copies stay asynchronous) and
+    unregisters them afterwards; bitwise the same result as without registration."""
+    cfg = CONFIGS["c1"].scaled(3000, 3000, 128)
+    a, ac, b, bc, c = host_system(cfg)
+    assert a.nbytes >= 64 << 20
+    monkeypatch.setenv("RSYLV_B200_HOST_REGISTER", "1")
+    r1 = api.solve_tiled_robust(qt(a, ac), qt(b, bc), c, 128)
+    monkeypatch.setenv("RSYLV_B200_HOST_REGISTER", "0")
+    r0 = api.solve_tiled_robust(qt(a, ac), qt(b, bc), c, 128)
+    assert r1.alpha_exp == r0.alpha_exp and np.array_equal(r1.y, r0.y)
+    # registration is released: the same buffers can be registered again by the next call
+    monkeypatch.setenv("RSYLV_B200_HOST_REGISTER", "1")
+    r2 = api.solve_tiled_robust(qt(a, ac), qt(b, bc), c, 128)
+    assert np.array_equal(r2.y, r0.y)
