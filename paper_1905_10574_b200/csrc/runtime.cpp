@@ -863,18 +863,20 @@ static int solve_host_pipelined(rsylv_b200_ctx* ctx, const SolveArgs& H, double*
     return status;
 }
 
-// Page-locks the caller's host buffers for the duration of one rsylv_b200_solve (the reference's
-// DenseMatrix storage is ordinary pageable memory): cudaMemcpy*Async from pageable memory is
-// staged and blocks the host thread, which would serialize the host pipeline's per-column
-// copies ahead of the DAG launch instead of overlapping them with it. Buffers that are already
-// pinned / registered, or smaller than 64 MB, are left alone; RSYLV_B200_HOST_REGISTER=0 turns
-// it off.
+// Optionally page-locks the caller's host buffers for one rsylv_b200_solve (the reference's
+// DenseMatrix storage is ordinary pageable memory, whose cudaMemcpy*Async is staged and blocks
+// the host thread, so the host pipeline's per-column copies no longer overlap the DAG). Measured
+// at c4 (tools/e2e_pageable.py, profiles/r02/e2e_pageable_c4.jsonl): pinned 272 ms, pageable
+// 793 ms, pageable + cudaHostRegister for the call 1147 ms -- pinning 10 GB costs more than the
+// overlap it buys, so it is off unless RSYLV_B200_HOST_REGISTER=1 (worth it only for callers
+// that keep registering the same buffers themselves: pass pinned memory). Buffers that are
+// already pinned / registered, or smaller than 64 MB, are left alone.
 struct HostRegistration {
     std::vector<void*> regs;
-    bool enabled = true;
+    bool enabled = false;
     HostRegistration() {
         const char* e = std::getenv("RSYLV_B200_HOST_REGISTER");
-        enabled = !(e && e[0] == '0');
+        enabled = e && e[0] == '1';
     }
     void add(const void* p, size_t bytes, bool read_only) {
         if (!enabled || !p || bytes < ((size_t)64 << 20)) return;

@@ -138,9 +138,10 @@ print(r.alpha_exp)
 
 
 def test_pageable_buffers_page_locked_for_the_call(monkeypatch):
-    """The reference's DenseMatrix storage is pageable: rsylv_b200_solve page-locks buffers of
-    >= 64 MB for the call (so the host pipeline's per-column copies stay asynchronous) and
-    unregisters them afterwards; bitwise the same result as without registration."""
+    """The reference's DenseMatrix storage is pageable: with RSYLV_B200_HOST_REGISTER=1
+    rsylv_b200_solve page-locks buffers of >= 64 MB for the call (so the host pipeline's
+    per-column copies stay asynchronous) and unregisters them afterwards; bitwise the same
+    result as without registration (the default: pinning per call is not profitable)."""
     cfg = CONFIGS["c1"].scaled(3000, 3000, 128)
     a, ac, b, bc, c = host_system(cfg)
     assert a.nbytes >= 64 << 20

@@ -58,10 +58,10 @@ na, nb, nc = pa.numpy().copy(), pb.numpy().copy(), pc.numpy().copy()
 ny = np.zeros_like(nc)
 del pa, pb, pc
 os.environ["RSYLV_B200_HOST_REGISTER"] = "0"
-run((na, nb, nc, ny), "pageable, not registered")
+run((na, nb, nc, ny), "pageable, not registered (default)")
 y2 = ny.copy()
 os.environ["RSYLV_B200_HOST_REGISTER"] = "1"
 ny[:] = 0
-run((na, nb, nc, ny), "pageable, page-locked for the call (default)")
+run((na, nb, nc, ny), "pageable, page-locked for the call (RSYLV_B200_HOST_REGISTER=1)")
 assert np.array_equal(ny, y2) and np.array_equal(ny, y1.numpy()), "results differ"
 print(json.dumps({"bitwise_equal": True}))
