@@ -22,7 +22,7 @@ for name in sys.argv[1:] or ["c1"]:
         print("   per sub-block (per warp): solve %.2f us, norm %.2f us, count %d" % (out[5] / out[6] / 1965, out[7] / out[6] / 1965, out[6]))
     print("   column-path fallbacks to the exact sub-block solver: %d" % out[12])
     if out[22]:
-        print("   fast path per solver-warp call: urgent updates %.2f us, sub-block solve(s) %.2f us (%d calls); deferred updates %.1f us/tile summed over warps" % (out[20] / out[22] / 1965, out[21] / out[22] / 1965, out[22], out[23] / ntiles / 1965))
+        print("   fast path per solver-warp call: urgent updates %.2f us, sub-block solve(s) %.2f us (%d calls), immediate repeat %.2f us; deferred updates %.1f us/tile summed over warps" % (out[20] / out[22] / 1965, out[21] / out[22] / 1965, out[22], out[24] / out[22] / 1965, out[23] / ntiles / 1965))
     print("   fast diagonal-tile attempt: %.1f us/tile in its wavefront, %d of %d tiles fell back to the exact path" % (out[14] / ntiles / 1965, out[15], ntiles))
     print("   flag-wait=%.1f us/tile, metadata-arrival=%.1f us/tile, header=%.1f us/tile, chunks=%d prescaled=%d (%.1f%%)" % (out[9] / ntiles / 1965, out[14] / ntiles / 1965, out[13] / ntiles / 1965, out[10], out[11], 100.0 * out[11] / max(1, out[10])))
     nw = ntiles * 16 * 1965

@@ -199,6 +199,43 @@ __global__ void k_solve_gen(int reps, double* Cg, const double* Ag, const double
     if (!ok) atomicAdd(okout, 1);
 }
 
+#ifndef KSDL_BOUNDS
+#define KSDL_BOUNDS __launch_bounds__(512, 1)
+#endif
+// The DAG's layout for fast_subsolve_1x1: the sub-block inside a 128 x 129 tile at (r0, c0), the
+// A / B diagonal sub-blocks in the SSmem arrays, 16 warps of which `nact` call the solver (the
+// others wait at the barrier, like the DAG's non-solver warps).
+template <int kSepW>
+__global__ void KSDL_BOUNDS k_solve_daglayout(int nact, int reps, const double* Cg,
+                                                          const double* Ag, const double* Bg,
+                                                          long long* cyc) {
+    extern __shared__ double sh[];
+    double* T = sh;                            // 128 x 129
+    double* Ad = T + 128 * 129;                // 9 x 16 x 16
+    double* Bd = Ad + 9 * 16 * 16;             // 9 x 16 x 17
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    long long tot = 0;
+    for (int rep = 0; rep < reps; ++rep) {
+        for (int e = threadIdx.x; e < 128 * 128; e += blockDim.x) T[(e & 127) + (e >> 7) * 129] = Cg[e & 255];
+        for (int e = threadIdx.x; e < 9 * 256; e += blockDim.x) {
+            const int p = e / 256, r = e % 16, c = (e / 16) % 16;
+            Ad[p * 256 + r + c * 16] = Ag[r + c * 16];
+            Bd[p * 272 + r + c * 17] = Bg[r + c * 16];
+        }
+        __syncthreads();
+        const long long t0 = clock64();
+        if (warp < nact) {
+            // sub-blocks on anti-diagonal 7 of the 8 x 8 grid: (pb, qb) = (7 - it... ) like the DAG
+            const int qb = warp, pb = 7 - (7 - qb);  // (pb = qb: diagonal positions)
+            double* W = kSepW ? T + warp * 16 * 129 : T + pb * 16 + qb * 16 * 129;
+            rsb::fast_subsolve_1x1(W, Ad + pb * 256, Bd + qb * 272, 16, 16, 1e-290, 1e300);
+        }
+        __syncthreads();
+        tot += clock64() - t0;
+    }
+    if (threadIdx.x == 0) cyc[0] = tot / reps;
+}
+
 // ---------------------------------------------------------------------------- host
 static void cpu_solve(const double* A, const double* B, double* C) {
     // 1x1 blocks: X(r,c) = (C(r,c) - sum_{p>r} A(r,p) X(p,c) - sum_{q<c} X(r,q) B(q,c)) / (A(r,r)+B(c,c))
@@ -288,6 +325,21 @@ int main(int argc, char** argv) {
             printf("skew16 variant %d (B %s%s) nw=%d: %lld cycles per warp (2 sub-blocks), max rel err %.2e, fails %d %s\n",
                    variant, (variant & 1) ? "lds" : "shfl", variant >= 2 ? ", window" : "", nw, mx, err, okc, cudaGetErrorString(e));
         }
+    {   // the DAG's layout and warp population
+        const size_t shb = (128 * 129 + 9 * 256 + 9 * 272) * 8;
+        for (int sep = 0; sep < 2; ++sep) {
+            auto kf = sep ? k_solve_daglayout<1> : k_solve_daglayout<0>;
+            cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb);
+            for (int nact : {1, 4}) {
+                kf<<<1, 512, shb>>>(nact, 1, dC, dA, dB, dcyc);
+                kf<<<1, 512, shb>>>(nact, 20, dC, dA, dB, dcyc);
+                cudaError_t e = cudaDeviceSynchronize();
+                long long h = 0;
+                cudaMemcpy(&h, dcyc, 8, cudaMemcpyDeviceToHost);
+                printf("daglayout%s 1x1 nact=%d (16 warps): %lld cycles per call %s\n", sep ? "(W separate)" : "", nact, h, cudaGetErrorString(e));
+            }
+        }
+    }
     // ---- mixed blocks: dense Kronecker reference
     {
         const int nb = 4;
