@@ -135,7 +135,14 @@ def cmd_tune(args) -> int:
     nu = float(args.n) if args.nu < 0 else args.nu
     a, ac, b, bc, c = _system(args, mu, nu)
     rows, best_tile, best = [], 0, math.inf
-    for ts in range(args.tile_min, args.tile_max + 1, args.tile_step):
+    sizes = list(range(args.tile_min, args.tile_max + 1, args.tile_step))
+    above = [ts for ts in sizes if ts > api.INTERNAL_TILE]
+    if above:
+        # the device serves every request above 128 with 128-tiles (one CTA per tile): those
+        # sizes run the same partition and time the same; they stay in the CSV for the record
+        print(f"note: tile sizes {above[0]}..{above[-1]} exceed the internal tile "
+              f"({api.INTERNAL_TILE}) and are served by {api.INTERNAL_TILE}-tiles", file=sys.stderr)
+    for ts in sizes:
         args.tile_size = ts
         _run_once(args, mu, nu, args.workers[0], a, ac, b, bc, c)  # untimed warm-up
         first = len(rows)
