@@ -20,6 +20,9 @@ constexpr int kBM = 128;         // internal tile edge: one CTA task owns one <=
 constexpr int kTileMax = kBM;    // largest internal tile edge
 // max sub-blocks per tile edge (tile <= 128, sub-blocks >= kSub - 1)
 constexpr int kSubMax = (kBM + kSub - 2) / (kSub - 1);
+constexpr int kFS = 8;                                 // fast-path sub-block edge
+constexpr int kFSMax = (kBM + kFS - 2) / (kFS - 1);    // fast-path sub-blocks per tile edge
+constexpr int kFLA = 8, kFLB = 9;                      // fast-path staged A / B leading dims
 constexpr int kLDT = kBM + 1;    // shared-memory tile leading dim (odd: conflict-free columns)
 constexpr int kLDD = kSub + 1;   // staged diagonal sub-block of B leading dim (column reads across lanes)
 constexpr int kLDDA = kSub;      // staged diagonal sub-block of A: row reads across lanes (r0 + 16 c: distinct banks)

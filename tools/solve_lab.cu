@@ -7,7 +7,6 @@
 #include <vector>
 
 #define FULL 0xffffffffu
-#include "../paper_1905_10574_b200/csrc/kernels.cu"  // fast_subsolve_1x1 / _gen
 
 // ---------------------------------------------------------------------------- probes
 // nw warps, each issues n independent (4 chains) 64-bit shuffles / LDS.64 / DFMA.
@@ -157,8 +156,7 @@ __global__ void k_solve(int nblk, int reps, double* Cg, const double* Ag, const 
         if (kVariant == 1) ok &= skew16<true>(W, A, B, 16, 16, 1e-290, 1e300);
         if (kVariant == 2) ok &= skew16<false, true>(W, A, B, 16, 16, 1e-290, 1e300);
         if (kVariant == 3) ok &= skew16<true, true>(W, A, B, 16, 16, 1e-290, 1e300);
-        if (kVariant == 4) ok &= rsb::fast_subsolve_1x1(W, A, B, 16, 16, 1e-290, 1e300);
-        if (kVariant == 5) ok &= rsb::fast_subsolve_gen(W, A, B, codes1, codes1, 16, 16, 1e-290, 1e300);
+
         __syncwarp();
         tot += clock64() - t0;
         if (rep == 0 && lane == 0) cyc[64 + blockIdx.x * nw + warp] = clock64() - t0;
@@ -168,52 +166,24 @@ __global__ void k_solve(int nblk, int reps, double* Cg, const double* Ag, const 
     if (!ok) atomicAdd(okout, 1);
 }
 
-// one mixed sub-block per warp (fast_subsolve_gen)
-__global__ void k_solve_gen(int reps, double* Cg, const double* Ag, const double* Bg,
-                            const unsigned char* rc, const unsigned char* cc, long long* cyc,
-                            int* okout) {
-    extern __shared__ double sh[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nw = blockDim.x >> 5;
-    double* W = sh + warp * 16 * LDW;
-    double* A = sh + nw * 16 * LDW + warp * 16 * LDA;
-    double* B = sh + nw * 16 * (LDW + LDA) + warp * 16 * LDB;
-    const int blk = blockIdx.x * nw + warp;
-    long long tot = 0;
-    bool ok = true;
-    for (int rep = 0; rep < reps; ++rep) {
-        for (int e = lane; e < 256; e += 32) {
-            const int r = e & 15, c = e >> 4;
-            W[r + c * LDW] = Cg[(long long)blk * 256 + e];
-            A[r + c * LDA] = Ag[(long long)blk * 256 + e];
-            B[r + c * LDB] = Bg[(long long)blk * 256 + e];
-        }
-        __syncwarp();
-        const long long t0 = clock64();
-        ok &= rsb::fast_subsolve_gen(W, A, B, rc + blk * 16, cc + blk * 16, 16, 16, 1e-290, 1e300);
-        __syncwarp();
-        tot += clock64() - t0;
-    }
-    for (int e = lane; e < 256; e += 32) Cg[(long long)blk * 256 + e] = W[(e & 15) + (e >> 4) * LDW];
-    if (lane == 0) cyc[blockIdx.x * nw + warp] = tot / reps;
-    if (!ok) atomicAdd(okout, 1);
-}
-
 #ifndef KSDL_BOUNDS
 #define KSDL_BOUNDS __launch_bounds__(512, 1)
 #endif
-// The DAG's layout for fast_subsolve_1x1: the sub-block inside a 128 x 129 tile at (r0, c0), the
-// A / B diagonal sub-blocks in the SSmem arrays, 16 warps of which `nact` call the solver (the
-// others wait at the barrier, like the DAG's non-solver warps).
+// The DAG's layout for a 16-wide register-wavefront solve: the sub-block inside a 128 x 129 tile
+// at (r0, c0), A / B diagonal sub-blocks in 9 x 16 x 16 / 9 x 16 x 17 arrays, 16 warps of which
+// `nact` solve (the others wait at the barrier, like the DAG's non-solver warps). Round 2 ran the
+// package's 16-wide fast_subsolve_1x1 here: 13.9 k cycles per call when the compiler may use 165
+// registers (-DKSDL_BOUNDS=), 37.5 k under __launch_bounds__(512, 1) (125 registers).
+// skew16<true, true> is the same algorithm in this file.
 template <int kSepW>
 __global__ void KSDL_BOUNDS k_solve_daglayout(int nact, int reps, const double* Cg,
-                                                          const double* Ag, const double* Bg,
-                                                          long long* cyc) {
+                                              const double* Ag, const double* Bg,
+                                              long long* cyc) {
     extern __shared__ double sh[];
     double* T = sh;                            // 128 x 129
     double* Ad = T + 128 * 129;                // 9 x 16 x 16
     double* Bd = Ad + 9 * 16 * 16;             // 9 x 16 x 17
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
     long long tot = 0;
     for (int rep = 0; rep < reps; ++rep) {
         for (int e = threadIdx.x; e < 128 * 128; e += blockDim.x) T[(e & 127) + (e >> 7) * 129] = Cg[e & 255];
@@ -225,10 +195,9 @@ __global__ void KSDL_BOUNDS k_solve_daglayout(int nact, int reps, const double* 
         __syncthreads();
         const long long t0 = clock64();
         if (warp < nact) {
-            // sub-blocks on anti-diagonal 7 of the 8 x 8 grid: (pb, qb) = (7 - it... ) like the DAG
-            const int qb = warp, pb = 7 - (7 - qb);  // (pb = qb: diagonal positions)
+            const int qb = warp, pb = qb;
             double* W = kSepW ? T + warp * 16 * 129 : T + pb * 16 + qb * 16 * 129;
-            rsb::fast_subsolve_1x1(W, Ad + pb * 256, Bd + qb * 272, 16, 16, 1e-290, 1e300);
+            skew16<true, true>(W, Ad + pb * 256, Bd + qb * 272, 16, 16, 1e-290, 1e300);
         }
         __syncthreads();
         tot += clock64() - t0;
@@ -296,12 +265,12 @@ int main(int argc, char** argv) {
     cudaMemset(dcodes, 1, 64);
     cudaMemcpy(dA, A.data(), A.size() * 8, cudaMemcpyHostToDevice);
     cudaMemcpy(dB, B.data(), B.size() * 8, cudaMemcpyHostToDevice);
-    for (int variant = 3; variant < 5; ++variant)
+    for (int variant = 0; variant < 4; ++variant)
         for (int nw : {1, 4}) {
             const size_t shb = (size_t)nw * 2 * 16 * (LDW + LDA + LDB) * 8;
             cudaMemcpy(dC, C.data(), C.size() * 8, cudaMemcpyHostToDevice);
             cudaMemset(dok, 0, 4);
-            auto kf = variant == 0 ? k_solve<0> : variant == 1 ? k_solve<1> : variant == 2 ? k_solve<2> : variant == 3 ? k_solve<3> : variant == 4 ? k_solve<4> : k_solve<5>;
+            auto kf = variant == 0 ? k_solve<0> : variant == 1 ? k_solve<1> : variant == 2 ? k_solve<2> : k_solve<3>;
             cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb);
             kf<<<1, 32 * nw, shb>>>(nw * 2, 1, dC, dA, dB, dcyc, dok, dcodes);
             cudaDeviceSynchronize();
@@ -338,98 +307,6 @@ int main(int argc, char** argv) {
                 cudaMemcpy(&h, dcyc, 8, cudaMemcpyDeviceToHost);
                 printf("daglayout%s 1x1 nact=%d (16 warps): %lld cycles per call %s\n", sep ? "(W separate)" : "", nact, h, cudaGetErrorString(e));
             }
-        }
-    }
-    // ---- mixed blocks: dense Kronecker reference
-    {
-        const int nb = 4;
-        std::vector<double> GA(nb * 256, 0.0), GB(nb * 256, 0.0), GC(nb * 256), GX;
-        std::vector<unsigned char> rc(nb * 16), cc(nb * 16);
-        auto codes = [&](unsigned char* cd) {
-            int p = 0;
-            while (p < 16) {
-                if (p + 1 < 16 && rand() % 2) { cd[p] = 2; cd[p + 1] = 0; p += 2; }
-                else { cd[p] = 1; p += 1; }
-            }
-        };
-        auto qt = [&](double* M, const unsigned char* cd) {
-            for (int c = 0; c < 16; ++c)
-                for (int r = 0; r < 16; ++r) M[r + c * 16] = r < c ? u() : 0.0;
-            for (int c = 0; c < 16; ++c) {
-                if (cd[c] == 0) continue;
-                const double a = 1.25 + 0.75 * u();
-                M[c + c * 16] = a;
-                if (cd[c] == 2) {
-                    M[(c + 1) + (c + 1) * 16] = a;
-                    M[c + (c + 1) * 16] = 0.55 + 0.45 * u();
-                    M[(c + 1) + c * 16] = -(0.55 + 0.45 * u());
-                }
-            }
-        };
-        for (int b = 0; b < nb; ++b) {
-            codes(&rc[b * 16]);
-            codes(&cc[b * 16]);
-            qt(&GA[b * 256], &rc[b * 16]);
-            qt(&GB[b * 256], &cc[b * 16]);
-            for (int e = 0; e < 256; ++e) GC[b * 256 + e] = u();
-        }
-        GX = GC;
-        for (int b = 0; b < nb; ++b) {  // K x = c, K = I (x) A + B^T (x) I, x = vec(X)
-            std::vector<double> K(256 * 256, 0.0), x(256);
-            for (int c = 0; c < 16; ++c)
-                for (int r = 0; r < 16; ++r) {
-                    const int row = r + 16 * c;
-                    for (int p = 0; p < 16; ++p) K[row * 256 + p + 16 * c] += GA[b * 256 + r + p * 16];
-                    for (int l = 0; l < 16; ++l) K[row * 256 + r + 16 * l] += GB[b * 256 + l + c * 16];
-                    x[row] = GC[b * 256 + row];
-                }
-            for (int k = 0; k < 256; ++k) {
-                int pv = k;
-                for (int i = k + 1; i < 256; ++i) if (fabs(K[i * 256 + k]) > fabs(K[pv * 256 + k])) pv = i;
-                for (int j = 0; j < 256; ++j) std::swap(K[k * 256 + j], K[pv * 256 + j]);
-                std::swap(x[k], x[pv]);
-                for (int i = k + 1; i < 256; ++i) {
-                    const double f = K[i * 256 + k] / K[k * 256 + k];
-                    for (int j = k; j < 256; ++j) K[i * 256 + j] -= f * K[k * 256 + j];
-                    x[i] -= f * x[k];
-                }
-            }
-            for (int k = 255; k >= 0; --k) {
-                double v = x[k];
-                for (int j = k + 1; j < 256; ++j) v -= K[k * 256 + j] * x[j];
-                x[k] = v / K[k * 256 + k];
-            }
-            for (int e = 0; e < 256; ++e) GX[b * 256 + e] = x[e];
-        }
-        double *dGA, *dGB, *dGC;
-        unsigned char *drc, *dcc;
-        cudaMalloc(&dGA, GA.size() * 8); cudaMalloc(&dGB, GB.size() * 8); cudaMalloc(&dGC, GC.size() * 8);
-        cudaMalloc(&drc, rc.size()); cudaMalloc(&dcc, cc.size());
-        cudaMemcpy(dGA, GA.data(), GA.size() * 8, cudaMemcpyHostToDevice);
-        cudaMemcpy(dGB, GB.data(), GB.size() * 8, cudaMemcpyHostToDevice);
-        cudaMemcpy(drc, rc.data(), rc.size(), cudaMemcpyHostToDevice);
-        cudaMemcpy(dcc, cc.data(), cc.size(), cudaMemcpyHostToDevice);
-        for (int nw : {1, 4}) {
-            const size_t shb = (size_t)nw * 16 * (LDW + LDA + LDB) * 8;
-            cudaFuncSetAttribute(k_solve_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb);
-            cudaMemcpy(dGC, GC.data(), GC.size() * 8, cudaMemcpyHostToDevice);
-            cudaMemset(dok, 0, 4);
-            k_solve_gen<<<1, 32 * nw, shb>>>(1, dGC, dGA, dGB, drc, dcc, dcyc, dok);
-            cudaDeviceSynchronize();
-            std::vector<double> G(GC.size());
-            cudaMemcpy(G.data(), dGC, G.size() * 8, cudaMemcpyDeviceToHost);
-            double err = 0, mx = 0;
-            for (int i = 0; i < nw * 256; ++i) { err = fmax(err, fabs(G[i] - GX[i])); mx = fmax(mx, fabs(GX[i])); }
-            cudaMemcpy(dGC, GC.data(), GC.size() * 8, cudaMemcpyHostToDevice);
-            k_solve_gen<<<1, 32 * nw, shb>>>(20, dGC, dGA, dGB, drc, dcc, dcyc, dok);
-            cudaError_t e = cudaDeviceSynchronize();
-            std::vector<long long> h(nw);
-            cudaMemcpy(h.data(), dcyc, 8 * nw, cudaMemcpyDeviceToHost);
-            long long m = 0;
-            for (long long v : h) m = v > m ? v : m;
-            int okc = 0;
-            cudaMemcpy(&okc, dok, 4, cudaMemcpyDeviceToHost);
-            printf("gen nw=%d: %lld cycles per warp (1 mixed sub-block), max abs err / max %.2e, fails %d %s\n", nw, m, err / mx, okc, cudaGetErrorString(e));
         }
     }
     return 0;
