@@ -8,6 +8,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>  // CUtensorMap (type only: the encoder is resolved at run time, no libcuda link)
 #include <cuda_runtime.h>
 
 namespace rsb {
@@ -254,6 +255,9 @@ struct Problem {
     const int* ccut;            // N+1 col-tile cuts
     const unsigned char* ablk;  // m block codes
     const unsigned char* bblk;  // n block codes
+    const CUtensorMap* tmaps;   // device array of 4 TMA tensor maps over the packed slots:
+                                // [0] Apack as L operand, [1] Ypack as L, [2] Ypack as R,
+                                // [3] Bpack as R (runtime.cpp make_tmaps; kernels.cu USmem)
     const double* Apack;        // upper tiles of A, slot tri(i,k) = k*(k+1)/2 + i
     const double* Bpack;        // upper tiles of B
     double* Ypack;              // all tiles of Y, slot i*N + j

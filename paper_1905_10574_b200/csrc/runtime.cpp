@@ -69,6 +69,62 @@ T* buf(rsylv_b200_ctx* ctx, const char* name, size_t count) {
     return static_cast<T*>(b.p);
 }
 
+// TMA tensor maps of the update GEMM's operand ring (kernels.cu USmem). A slot array (column-
+// major 128 x 128 slots, `nslots` of them) is viewed as a 3-D tensor: dim0 = 8 consecutive rows
+// (8 B stride), dim1 = column over all slots (1 KB stride), dim2 = row group of 8 (64 B stride).
+// An L operand chunk (128 rows x kKC k) is the box {8, kKC, 16} at (0, slot*128 + k0, 0), an R
+// operand chunk (kKC k x 128 columns) the box {8, 128, kKC/8} at (0, slot*128, k0/8); both land
+// in shared memory with SWIZZLE_64B, which makes every DMMA fragment load conflict-free.
+// cuTensorMapEncodeTiled is resolved through the runtime (no link against libcuda).
+typedef CUresult (*TmapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+void encode_slot_map(rsylv_b200_ctx* ctx, CUtensorMap* map, const double* base, size_t nslots,
+                     bool as_left) {
+    static TmapEncodeFn enc = nullptr;
+    if (!enc) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        ck(ctx, cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q),
+           "cuTensorMapEncodeTiled entry point");
+        if (q != cudaDriverEntryPointSuccess || !fn) {
+            ctx->last_error = "cuTensorMapEncodeTiled not available in this driver";
+            throw Fail{RSYLV_CUDA_ERROR};
+        }
+        enc = reinterpret_cast<TmapEncodeFn>(fn);
+    }
+    const cuuint64_t dims[3] = {8, (cuuint64_t)std::max<size_t>(nslots, 1) * kBM, kBM / 8};
+    const cuuint64_t strides[2] = {(cuuint64_t)kBM * 8, 64};
+    const cuuint32_t box[3] = {8, (cuuint32_t)(as_left ? kKC : kBM),
+                               (cuuint32_t)(as_left ? kBM / 8 : kKC / 8)};
+    const cuuint32_t es[3] = {1, 1, 1};
+    const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        ctx->last_error = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+        throw Fail{RSYLV_CUDA_ERROR};
+    }
+}
+
+// the four maps of one rank's Problem, copied to the device buffer `name`
+const CUtensorMap* make_tmaps(rsylv_b200_ctx* ctx, const char* name, const double* Ap, size_t na,
+                              const double* Bp, size_t nb, const double* Yp, size_t ny,
+                              cudaStream_t st) {
+    CUtensorMap h[4];
+    encode_slot_map(ctx, &h[0], Ap, na, true);
+    encode_slot_map(ctx, &h[1], Yp, ny, true);
+    encode_slot_map(ctx, &h[2], Yp, ny, false);
+    encode_slot_map(ctx, &h[3], Bp, nb, false);
+    CUtensorMap* d = buf<CUtensorMap>(ctx, name, 4);
+    ck(ctx, cudaMemcpyAsync(d, h, sizeof(h), cudaMemcpyHostToDevice, st), "tmaps h2d");
+    ck(ctx, cudaStreamSynchronize(st), "sync");  // h goes out of scope
+    return d;
+}
+
 // Tile partition: cut at running multiples of ts; a cut that would split a 2x2 block moves
 // one index EARLIER (the reference moves it later, partition.cpp:74-91; Y/alpha does not depend
 // on the partition and earlier cuts keep every tile within one padded slot).
@@ -123,6 +179,7 @@ struct RankBufs {
     int* tnext = nullptr;
     int* tasks = nullptr;
     int ntasks = 0;
+    const CUtensorMap* tmaps = nullptr;  // TMA views of Apack / Ypack / Bpack for this rank
 };
 
 // Everything one solve needs between its phases (kept in the context for the dist_* calls).
@@ -293,6 +350,7 @@ int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std:
         ck(ctx, cudaMemsetAsync(B.err, 0, 4 * sizeof(int), st), "memset");
         ck(ctx, cudaMemsetAsync(B.ev, 0, 2 * sizeof(unsigned long long), st), "memset");
         ck(ctx, cudaMemsetAsync(B.tnext, 0, sizeof(int), st), "memset");
+        B.tmaps = make_tmaps(ctx, ("tmaps" + sfx).c_str(), Ap, na, Bp, nb, B.Yp, ny, st);
         Problem Q = P;
         Q.rank = r;  // (multi-rank: C packed for the owned tile columns only)
         Q.Ypack = B.Yp;
@@ -366,6 +424,7 @@ Problem rank_problem(rsylv_b200_ctx* ctx, size_t li) {
     const RankBufs& B = PL.rb[li];
     Problem Q = PL.base;
     Q.Ypack = B.Yp;
+    Q.tmaps = B.tmaps;
     Q.ynorm = B.ynorm;
     Q.yexp = B.yexp;
     Q.yst = B.yexp + (size_t)Q.M * Q.N;
@@ -1331,6 +1390,7 @@ int rsylv_b200_robust_update(rsylv_b200_ctx* ctx, size_t m, size_t k, size_t n, 
         P.err = errw;
         P.err_pivot = pivw;
         P.events = evw;
+        P.tmaps = make_tmaps(ctx, "rutmaps", Ap, 3, Bp, 1, Yp, 2, st);
         P.nsub_r = P.nsub_c = TSP / kBM;
         P.omega = omega > 0 ? omega : DBL_MAX / 2;
         P.small_num = DBL_MIN / DBL_EPSILON;
