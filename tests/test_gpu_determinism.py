@@ -86,3 +86,24 @@ def test_c5_full_size_bitwise_deterministic():
         assert st == st0 and r.alpha_exp == r0.alpha_exp
         # bitwise (int64 views: NaN-safe, -0.0 distinct)
         assert torch.equal(Y1.view(torch.int64), Y0.view(torch.int64))
+
+
+@pytest.mark.parametrize("name,size,reps", [("c5", 12000, 24), ("c2", 6000, 24)])
+def test_repeat_solves_bitwise_stress(name, size, reps):
+    """Race detector at a size where tiles chase their sources closely (many consumers open a
+    source right after its flag is set): every repeat solve must equal the first bit for bit,
+    events and alpha included. (Round 2: with the ring refilled a chunk earlier and only the
+    lookahead's acquire before the TMA reads, 5-15 % of these solves differed.)"""
+    import torch
+    from paper_1905_10574_b200 import api
+    from paper_1905_10574_b200.configs import CONFIGS, device_system
+    cfg = CONFIGS[name].scaled(size)
+    A, ac, B, bc, C = device_system(cfg, torch)
+    Y0 = torch.empty((cfg.n, cfg.m), dtype=torch.float64, device="cuda").T
+    st0, r0 = api.solve_tiled_robust_device(A, ac, B, bc, C, Y0, cfg.tile, raise_underflow=False)
+    Y1 = torch.empty_like(Y0)
+    for k in range(reps):
+        Y1.fill_(float("nan"))
+        st, r = api.solve_tiled_robust_device(A, ac, B, bc, C, Y1, cfg.tile, raise_underflow=False)
+        assert st == st0 and r.alpha_exp == r0.alpha_exp and r.scaling_events == r0.scaling_events, k
+        assert torch.equal(Y1.view(torch.int64), Y0.view(torch.int64)), f"repeat {k} differs"

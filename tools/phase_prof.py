@@ -29,3 +29,4 @@ for name in sys.argv[1:] or ["c1"]:
     print("   chunks with an accumulator shift %d (%.1f%%), skipped (not live) %d" % (out[18], 100.0 * out[18] / max(1, out[10]), out[19]))
     print(name, "dag_ms", round(res.dag_ms, 2), "tiles", ntiles, " ".join(
         f"{names[i]}={out[i] / ntiles / 1965:.1f}us({100 * out[i] / tot:.0f}%)" for i in range(5)))
+    print("   lookahead-ready sources %d, of which the flag was NOT set at the duty thread's own acquire: %d" % (out[26], out[25]))
