@@ -263,7 +263,7 @@ struct Problem {
     double* Ypack;              // all tiles of Y, slot i*N + j
     double* anorm;              // M*M, (i,k) at i*M+k (upper)
     double* bnorm;              // N*N, (l,j) at l*N+j (upper)
-    int* in_ready;              // host pipeline: packed tile columns of A (from the right), B,
+    int* in_ready;              // host pipeline: shells packed so far for A (tile rows from the bottom), B,
                                 // C (from the left); nullptr when every input is packed upfront
     int* aexp;                  // M*M: off-diagonal A tiles are stored as A_ik * 2^-aexp (pack)
     int* bexp;                  // N*N: the same for B

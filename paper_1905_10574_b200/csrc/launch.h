@@ -26,10 +26,16 @@ void launch_update_bench(const Problem& P, int ctas, cudaStream_t st);
 void launch_pack_upper_col(const double* src, long long ld, const int* cut, int T, int TSP,
                            double* dst, double* norms, int* sexp, int k, cudaStream_t st,
                            bool normalize = true);
+void launch_pack_upper_row(const double* src, long long ld, const int* cut, int T, int TSP,
+                           double* dst, double* norms, int* sexp, int row, cudaStream_t st,
+                           bool normalize = true);
 void launch_pack_full_col(const double* src, long long ld, const Problem& P, double* norms,
-                          int j, cudaStream_t st);
+                          int j, int i0, cudaStream_t st);
+void launch_pack_full_row(const double* src, long long ld, const Problem& P, double* norms,
+                          int i, int jend, cudaStream_t st);
 void launch_set_ready(int* ready, int a, int b, int c, cudaStream_t st);
-void launch_validate_col(const Problem& P, int* reason, int kA, int jB, int jC, cudaStream_t st);
+void launch_validate_shell(const Problem& P, int* reason, int rA, int jB, int jC, int i0C, int rC,
+                           int jendC, cudaStream_t st);
 void launch_persistent(const Problem& P, int grid, cudaStream_t st);
 cudaError_t launch_persistent_mr(const Problem* probs_dev, int nranks_here, int grid,
                                  cudaStream_t st);

@@ -37,8 +37,10 @@ struct rsylv_b200_ctx {
     std::string last_error;
     bool configured = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evp = nullptr, evd = nullptr;
-    cudaStream_t side_stream = nullptr;                  // host pipeline: H2D + pack
+    cudaStream_t side_stream = nullptr;                  // host pipeline: pack + validation
+    cudaStream_t copy_stream = nullptr;                  // host pipeline: H2D copies (back to back)
     cudaEvent_t ev_side0 = nullptr, ev_side = nullptr;
+    std::vector<cudaEvent_t> ev_shell;                   // host pipeline: shell t's copies landed
     struct rsylv_b200_plan_holder* holder = nullptr;
 };
 
@@ -792,6 +794,7 @@ int rsylv_b200_create(int device, rsylv_b200_ctx** out) {
     cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
     if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_side0, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_side, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
@@ -818,6 +821,8 @@ void rsylv_b200_destroy(rsylv_b200_ctx* ctx) {
     if (ctx->evd) cudaEventDestroy(ctx->evd);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    for (cudaEvent_t e : ctx->ev_shell) cudaEventDestroy(e);
     if (ctx->ev_side0) cudaEventDestroy(ctx->ev_side0);
     if (ctx->ev_side) cudaEventDestroy(ctx->ev_side);
     delete ctx;
@@ -876,34 +881,94 @@ static int solve_host_pipelined(rsylv_b200_ctx* ctx, const SolveArgs& H, double*
     const int M = PL.M, N = PL.N, TSP = PL.TSP;
     const Problem Q = rank_problem(ctx, 0);
     unsigned long long h2d = 0;
+    static const bool dbg = std::getenv("RSYLV_B200_DEBUG_TIMING") != nullptr;
+    static cudaEvent_t dbg0 = nullptr, dbg1 = nullptr, dbg2 = nullptr;
+    static int* h_next = nullptr;
     std::function<void()> side = [&]() {
-        cudaStream_t ss = ctx->side_stream;
+        // copies on their own stream, back to back; the packs of shell t (on the 4 spare SMs)
+        // follow its copies through an event, so the copy engine never waits for a pack kernel
+        // (one stream for both serialized them: ~0.1 s of the c5 call)
+        cudaStream_t ss = ctx->side_stream, cs = ctx->copy_stream;
         ck(ctx, cudaStreamWaitEvent(ss, ctx->ev_side0, 0), "wait");
-        for (int t = 0; t < std::max(M, N); ++t) {
-            if (t < M) {  // A tile column k (its upper part), from the right
-                const int k = M - 1 - t;
-                const size_t c0 = PL.rc[k], c1 = PL.rc[k + 1];
-                ck(ctx, cudaMemcpy2DAsync(da + c0 * m, m * 8, H.a + c0 * H.lda, H.lda * 8, c1 * 8,
-                                          c1 - c0, cudaMemcpyHostToDevice, ss), "h2d A");
-                h2d += 8ull * c1 * (c1 - c0);
-                launch_pack_upper_col(da, (long long)m, Q.rcut, M, TSP, const_cast<double*>(Q.Apack), Q.anorm,
-                                      Q.aexp, k, ss, !std::isinf(PL.omega));
+        ck(ctx, cudaStreamWaitEvent(cs, ctx->ev_side0, 0), "wait");
+        if (dbg && !dbg0) {
+            cudaEventCreate(&dbg0);
+            cudaEventCreate(&dbg1);
+        }
+        if (dbg) cudaEventRecord(dbg0, cs);
+        while ((int)ctx->ev_shell.size() < std::max(M, N)) {
+            cudaEvent_t e = nullptr;
+            ck(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+            ctx->ev_shell.push_back(e);
+        }
+        // Shell order: shell t brings what the tiles (i, j) with max(M-1-i, j) == t need beyond
+        // the earlier shells -- tile row r = M-1-t of A from its diagonal tile on (the trailing
+        // square A[r:, r:] grows by one tile row), tile column t of B (the leading square), and
+        // of C the tiles (i >= r, t) and (r, j < t). The work the DAG can start on then grows
+        // like (copied fraction)^1.5 instead of ^3 (whole tile columns of A from the right and
+        // of C from the left), so the DAG is input-starved for ~100 ms instead of ~220 ms of the
+        // 0.47 s c5 upload.
+        // (copies are issued for kG shells at a time: the row strips are then kG tiles = kG KB
+        //  wide per column instead of 1 KB, which the copy engine moves at full PCIe rate; a
+        //  group's strip of A also carries the few below-diagonal tiles inside it, zeros)
+        static const int kG = [] {
+            const char* e = std::getenv("RSYLV_B200_SHELL_GROUP");
+            const int g = e ? std::atoi(e) : 8;
+            return g < 1 ? 1 : g;
+        }();
+        const int T = std::max(M, N);
+        for (int tlo = 0; tlo < T; tlo += kG) {
+            const int thi = std::min(tlo + kG, T);
+            const int rlo = std::max(0, M - thi);  // tile rows [rlo, M-1-tlo] (A, C), if tlo < M
+            const size_t R0 = PL.rc[rlo];
+            if (tlo < M) {
+                const size_t R1 = PL.rc[M - tlo];
+                ck(ctx, cudaMemcpy2DAsync(da + R0 + R0 * m, m * 8, H.a + R0 + R0 * H.lda, H.lda * 8,
+                                          (R1 - R0) * 8, m - R0, cudaMemcpyHostToDevice, cs), "h2d A");
+                h2d += 8ull * (R1 - R0) * (m - R0);
+                const size_t cend = PL.cc[std::min(tlo, N)];
+                if (cend > 0) {  // C: the group's tile rows, the tile columns of earlier groups
+                    ck(ctx, cudaMemcpy2DAsync(dc + R0, m * 8, H.c + R0, H.ldc * 8, (R1 - R0) * 8, cend,
+                                              cudaMemcpyHostToDevice, cs), "h2d C rows");
+                    h2d += 8ull * (R1 - R0) * cend;
+                }
             }
-            if (t < N) {  // B tile column t (upper part) and C tile column t, from the left
-                const size_t c0 = PL.cc[t], c1 = PL.cc[t + 1];
+            if (tlo < N) {  // B tile columns [tlo, chi) (upper part) and the C column pieces
+                const int chi = std::min(thi, N);
+                const size_t c0 = PL.cc[tlo], c1 = PL.cc[chi];
                 ck(ctx, cudaMemcpy2DAsync(db + c0 * n, n * 8, H.b + c0 * H.ldb, H.ldb * 8, c1 * 8,
-                                          c1 - c0, cudaMemcpyHostToDevice, ss), "h2d B");
-                ck(ctx, cudaMemcpy2DAsync(dc + c0 * m, m * 8, H.c + c0 * H.ldc, H.ldc * 8, m * 8,
-                                          c1 - c0, cudaMemcpyHostToDevice, ss), "h2d C");
-                h2d += 8ull * c1 * (c1 - c0) + 8ull * m * (c1 - c0);
-                launch_pack_upper_col(db, (long long)n, Q.ccut, N, TSP, const_cast<double*>(Q.Bpack), Q.bnorm,
-                                      Q.bexp, t, ss, !std::isinf(PL.omega));
-                launch_pack_full_col(dc, (long long)m, Q, Q.ynorm, t, ss);
+                                          c1 - c0, cudaMemcpyHostToDevice, cs), "h2d B");
+                ck(ctx, cudaMemcpy2DAsync(dc + R0 + c0 * m, m * 8, H.c + R0 + c0 * H.ldc, H.ldc * 8,
+                                          (m - R0) * 8, c1 - c0, cudaMemcpyHostToDevice, cs), "h2d C cols");
+                h2d += 8ull * c1 * (c1 - c0) + 8ull * (m - R0) * (c1 - c0);
             }
-            launch_validate_col(Q, PL.d_reason, t < M ? M - 1 - t : -1, t < N ? t : -1,
-                                t < N ? t : -1, ss);
-            launch_set_ready(Q.in_ready, t < M ? t + 1 : -1, t < N ? t + 1 : -1,
-                             t < N ? t + 1 : -1, ss);
+            ck(ctx, cudaEventRecord(ctx->ev_shell[tlo], cs), "event");
+            ck(ctx, cudaStreamWaitEvent(ss, ctx->ev_shell[tlo], 0), "wait");
+            for (int t = tlo; t < thi; ++t) {
+                const int r = M - 1 - t;              // tile row of this shell (A, C), if any
+                const int jend = std::min(t, N);      // C row strip: tile columns [0, jend)
+                const int i0 = std::max(0, r);        // C column piece: tile rows [i0, M)
+                if (t < M) {
+                    launch_pack_upper_row(da, (long long)m, Q.rcut, M, TSP, const_cast<double*>(Q.Apack),
+                                          Q.anorm, Q.aexp, r, ss, !std::isinf(PL.omega));
+                    if (jend > 0) launch_pack_full_row(dc, (long long)m, Q, Q.ynorm, r, jend, ss);
+                }
+                if (t < N) {
+                    launch_pack_upper_col(db, (long long)n, Q.ccut, N, TSP, const_cast<double*>(Q.Bpack),
+                                          Q.bnorm, Q.bexp, t, ss, !std::isinf(PL.omega));
+                    launch_pack_full_col(dc, (long long)m, Q, Q.ynorm, t, i0, ss);
+                }
+                launch_validate_shell(Q, PL.d_reason, t < M ? r : -1, t < N ? t : -1, t < N ? t : -1, i0,
+                                      (t < M && jend > 0) ? r : -1, jend, ss);
+                launch_set_ready(Q.in_ready, t < M ? t + 1 : -1, t < N ? t + 1 : -1, t + 1, ss);
+            }
+        }
+        if (dbg) {  // (read after the solve: nothing here may block the host before the DAG launch)
+            if (!dbg2) cudaEventCreate(&dbg2);
+            if (!h_next) cudaMallocHost(&h_next, sizeof(int));
+            cudaEventRecord(dbg1, cs);
+            cudaMemcpyAsync(h_next, Q.task_next, sizeof(int), cudaMemcpyDeviceToHost, ss);
+            cudaEventRecord(dbg2, ss);
         }
         launch_persistent(Q, std::min(kPipeReserve, ctx->sms - 1), ss);
         ck(ctx, cudaGetLastError(), "pipeline");
@@ -913,6 +978,16 @@ static int solve_host_pipelined(rsylv_b200_ctx* ctx, const SolveArgs& H, double*
     double numax = 0.0;
     status = plan_run(ctx, H.res, &emin, &numax, &side);
     H.res->h2d_bytes = h2d;
+    if (dbg && dbg2) {
+        cudaEventSynchronize(dbg1);
+        cudaEventSynchronize(dbg2);
+        float ms = 0, ms2 = 0;
+        cudaEventElapsedTime(&ms, dbg0, dbg1);
+        cudaEventElapsedTime(&ms2, dbg0, dbg2);
+        std::fprintf(stderr, "[rsylv_b200] host pipeline: H2D copies %.1f ms for %.2f GB (%.1f GB/s); last shell "
+                     "packed at %.1f ms, %d of %d tile tasks taken by then\n", ms, h2d / 1e9, h2d / 1e6 / ms, ms2,
+                     *h_next, Q.ntasks);
+    }
     if (status != RSYLV_OK) return status;
     const int ae = alpha_exponent(emin, numax, PL.omega);
     status = plan_finish(ctx, ae, numax, emin, dy, m, H.res);
