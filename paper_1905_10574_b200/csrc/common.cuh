@@ -293,6 +293,8 @@ struct Problem {
     // CUDA-IPC-mapped pointers) or virtual ranks sharing one GPU (sys_scope = 0).
     int fast_solve;             // diagonal-tile solve: 0 = exact sub-block path (default),
                                 // 1 = fast plain-FP64 attempt first + exact fallback
+    int issue_early;            // update ring: refill a stage before (1) / after (0) computing the
+                                // current chunk (kernels.cu update_phase; host: plan_prepare)
     int nranks, rank, sys_scope;
     double* peerY[kMaxRanks];
     int* peerYexp[kMaxRanks];

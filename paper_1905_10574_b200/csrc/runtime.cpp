@@ -310,6 +310,11 @@ int plan_prepare(rsylv_b200_ctx* ctx, const SolveArgs& A, int nranks, const std:
     P.x_omega = host_xf(PL.omega);
     P.x_target = host_xf(PL.omega * (1.0 - 0x1p-30));
     P.nranks = nranks;
+    {   // update ring refill order: early on throughput-bound DAGs (>= one tile per SM on the long
+        // anti-diagonals), late on latency-bound ones (RSYLV_B200_ISSUE_EARLY=0/1 overrides)
+        const char* ev = std::getenv("RSYLV_B200_ISSUE_EARLY");
+        P.issue_early = ev ? (ev[0] == '1') : (std::min(M, N) >= ctx->sms ? 1 : 0);
+    }
     {   // diagonal-tile solve path (RSYLV_B200_FAST_DIAG=1 opts in, for experiments)
         const char* ev = std::getenv("RSYLV_B200_FAST_DIAG");
         P.fast_solve = (A.opt.fast_diag || (ev && ev[0] == '1')) ? 1 : 0;
