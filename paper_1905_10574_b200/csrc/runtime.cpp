@@ -916,7 +916,7 @@ static int solve_host_pipelined(rsylv_b200_ctx* ctx, const SolveArgs& H, double*
         // (copies are issued for kG shells at a time: the row strips are then kG tiles = kG KB
         //  wide per column instead of 1 KB, which the copy engine moves at full PCIe rate; a
         //  group's strip of A also carries the few below-diagonal tiles inside it, zeros)
-        static const int kG = [] {
+        const int kG = [] {  // (read per call: tests vary it)
             const char* e = std::getenv("RSYLV_B200_SHELL_GROUP");
             const int g = e ? std::atoi(e) : 8;
             return g < 1 ? 1 : g;

@@ -1,6 +1,7 @@
-"""Host pipeline of rsylv_b200_solve (inputs streamed tile column by tile column while the DAG
-runs; include/rsylv_b200.h host_pipeline): results are bitwise those of the upfront path, and
-the argument checks keep the reference's order and reason codes."""
+"""Host pipeline of rsylv_b200_solve (inputs streamed in shells while the DAG runs -- tile row of
+A from its diagonal on, tile column of B, the matching L-shaped piece of C;
+include/rsylv_b200.h host_pipeline): results are bitwise those of the upfront path, and the
+argument checks keep the reference's order and reason codes."""
 import numpy as np
 import pytest
 
@@ -23,8 +24,14 @@ def _both(a, ac, b, bc, c, tile, cfg=None):
     return out
 
 
-@pytest.mark.parametrize("m,n,tile", [(300, 260, 32), (700, 650, 128), (129, 1000, 64)])
-def test_pipeline_bitwise_equals_upfront(m, n, tile):
+@pytest.mark.parametrize("group", [None, "1", "3"])
+@pytest.mark.parametrize("m,n,tile", [(300, 260, 32), (700, 650, 128), (129, 1000, 64), (1000, 129, 64),
+                                      (520, 40, 8)])
+def test_pipeline_bitwise_equals_upfront(m, n, tile, group, monkeypatch):
+    # (group: shells whose copies are issued together, runtime.cpp RSYLV_B200_SHELL_GROUP;
+    #  default 8, here also 1 and a size that does not divide the shell count)
+    if group is not None:
+        monkeypatch.setenv("RSYLV_B200_SHELL_GROUP", group)
     cfg = CONFIGS["c5"].scaled(m, n, tile)
     a, ac, b, bc, c = host_system(cfg)
     r0, r1 = _both(a, ac, b, bc, c, tile)
@@ -40,6 +47,23 @@ def test_pipeline_growth_system_matches_reference():
     mant, ex = np.frexp(d["alpha"])
     got = np.ldexp(r.y * mant, int(ex) - r.alpha_exp)
     assert golden.rel_inf_diff(got, d["y"]) <= 1e-12
+
+
+@pytest.mark.parametrize("pos", [(250, 3), (3, 250), (3, 100), (130, 130)])
+def test_pipeline_c_check_in_every_shell_piece(pos):
+    """A C entry above omega is caught wherever its tile travels: the column piece of an early
+    shell (bottom left), of the last shell (top right), a row strip, the corner tile."""
+    cfg = CONFIGS["c1"].scaled(256, 256, 32)
+    a, ac, b, bc, c = host_system(cfg)
+    c = c.copy(order="F")
+    c[pos] = 1e7
+    om = api.OverflowConfig(omega=1e6)
+    msgs = []
+    for hp in (1, -1):
+        with pytest.raises(ValueError) as e:
+            api.solve_tiled_robust(qt(a, ac), qt(b, bc), c, 32, om, host_pipeline=hp)
+        msgs.append(str(e.value))
+    assert "norm of C" in msgs[0] and msgs[0] == msgs[1]
 
 
 @pytest.mark.parametrize("which,reason", [("a", "norm of A"), ("b", "norm of B"), ("c", "norm of C")])
