@@ -490,12 +490,19 @@ Problem rank_problem(rsylv_b200_ctx* ctx, size_t li) {
 // side: host pipeline -- the DAG starts on all but kPipeReserve SMs, side() enqueues the H2D +
 // pack + validation work (and the remaining DAG CTAs) on the side stream, which the main
 // stream joins before the alpha reduction
-constexpr int kPipeReserve = 4;
+// RSYLV_B200_DEBUG_TIMING: events around the main DAG launch of the pipelined path
+static cudaEvent_t g_dbg_a = nullptr, g_dbg_b = nullptr;
+static int pipe_reserve() {  // SMs kept free of the main DAG launch for the pack kernels
+    const char* e = std::getenv("RSYLV_B200_PIPE_RESERVE");
+    const int r = e ? std::atoi(e) : 4;
+    return r < 1 ? 1 : r;
+}
+#define kPipeReserve pipe_reserve()
 // plan_launch enqueues the tile DAG (asynchronous); plan_collect waits for it and reduces.
 // plan_run = both. A single-process multi-GPU solve launches every device first, then collects
 // (a device's kernel waits on tiles its peers produce).
 int plan_launch(rsylv_b200_ctx* ctx, rsylv_b200_result* res,
-                const std::function<void()>* side = nullptr) {
+                const std::function<void(int)>* side = nullptr) {
     Plan& PL = ctx_plan(ctx);
     cudaStream_t st = PL.st;
     const int M = PL.M, N = PL.N;
@@ -513,14 +520,23 @@ int plan_launch(rsylv_b200_ctx* ctx, rsylv_b200_result* res,
                 res->dag_launches += 1;
             }
         } else if (side) {
-            // the side stream starts after the setup on st, NOT after the DAG launched below.
-            // Every producer (H2D, pack, validation, ready counters) is enqueued BEFORE the
-            // spinning DAG kernel: its progress then never depends on the two streams running
-            // concurrently (CUDA_LAUNCH_BLOCKING=1, compute-sanitizer or an MPS SM cap serialize
-            // them; the side stream's own DAG CTAs then solve everything)
+            // the side streams start after the setup on st, NOT after the DAG launched below.
+            // Serialized execution (CUDA_LAUNCH_BLOCKING=1, RSYLV_B200_SAFE_ORDER=1): every
+            // producer (H2D, pack, validation, ready counters) is enqueued BEFORE the spinning
+            // DAG kernel, whose progress then never depends on the streams running concurrently
+            // (the side stream's own DAG CTAs then solve everything). Otherwise only the first
+            // shells are enqueued before it and the rest right after the launch (side(1))
             ck(ctx, cudaEventRecord(ctx->ev_side0, st), "event");
-            (*side)();
+            (*side)(0);
+            const bool dbgt = std::getenv("RSYLV_B200_DEBUG_TIMING") != nullptr;
+            if (dbgt && !g_dbg_a) {
+                cudaEventCreate(&g_dbg_a);
+                cudaEventCreate(&g_dbg_b);
+            }
+            if (dbgt) cudaEventRecord(g_dbg_a, st);
             launch_persistent(P, std::max(1, ctx->sms - kPipeReserve), st);
+            if (dbgt) cudaEventRecord(g_dbg_b, st);
+            (*side)(1);
             ck(ctx, cudaStreamWaitEvent(st, ctx->ev_side, 0), "join");
             res->dag_launches = 2;
         } else {
@@ -631,7 +647,7 @@ int plan_collect(rsylv_b200_ctx* ctx, rsylv_b200_result* res, int* emin_out, dou
 }
 
 int plan_run(rsylv_b200_ctx* ctx, rsylv_b200_result* res, int* emin_out, double* numax_out,
-             const std::function<void()>* side = nullptr) {
+             const std::function<void(int)>* side = nullptr) {
     const int st = plan_launch(ctx, res, side);
     if (st != RSYLV_OK) return st;
     return plan_collect(ctx, res, emin_out, numax_out);
@@ -889,18 +905,28 @@ static int solve_host_pipelined(rsylv_b200_ctx* ctx, const SolveArgs& H, double*
     static const bool dbg = std::getenv("RSYLV_B200_DEBUG_TIMING") != nullptr;
     static cudaEvent_t dbg0 = nullptr, dbg1 = nullptr, dbg2 = nullptr;
     static int* h_next = nullptr;
-    std::function<void()> side = [&]() {
+    // phase 0: before the main DAG launch; phase 1: right after it. Enqueuing the later shells'
+    // 2-D copies costs the host ~0.1 s at c5 (one DMA descriptor per 8 KB strip row, up to 40000
+    // per copy), which used to delay the launch of the DAG kernel itself; now only the first
+    // shells (short strips) go before it. With CUDA_LAUNCH_BLOCKING=1 (or
+    // RSYLV_B200_SAFE_ORDER=1) every producer is still enqueued before the spinning kernel.
+    int next_tlo = 0;
+    bool side_done = false;
+    std::function<void(int)> side = [&](int phase) {
+        if (side_done) return;
         // copies on their own stream, back to back; the packs of shell t (on the 4 spare SMs)
         // follow its copies through an event, so the copy engine never waits for a pack kernel
         // (one stream for both serialized them: ~0.1 s of the c5 call)
         cudaStream_t ss = ctx->side_stream, cs = ctx->copy_stream;
-        ck(ctx, cudaStreamWaitEvent(ss, ctx->ev_side0, 0), "wait");
-        ck(ctx, cudaStreamWaitEvent(cs, ctx->ev_side0, 0), "wait");
+        if (phase == 0) {
+            ck(ctx, cudaStreamWaitEvent(ss, ctx->ev_side0, 0), "wait");
+            ck(ctx, cudaStreamWaitEvent(cs, ctx->ev_side0, 0), "wait");
+        }
         if (dbg && !dbg0) {
             cudaEventCreate(&dbg0);
             cudaEventCreate(&dbg1);
         }
-        if (dbg) cudaEventRecord(dbg0, cs);
+        if (dbg && phase == 0) cudaEventRecord(dbg0, cs);
         while ((int)ctx->ev_shell.size() < std::max(M, N)) {
             cudaEvent_t e = nullptr;
             ck(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -922,7 +948,15 @@ static int solve_host_pipelined(rsylv_b200_ctx* ctx, const SolveArgs& H, double*
             return g < 1 ? 1 : g;
         }();
         const int T = std::max(M, N);
-        for (int tlo = 0; tlo < T; tlo += kG) {
+        static const bool safe_order = [] {
+            const char* a = std::getenv("CUDA_LAUNCH_BLOCKING");
+            const char* b = std::getenv("RSYLV_B200_SAFE_ORDER");
+            return (a && a[0] == '1') || (b && b[0] == '1');
+        }();
+        // phase 0 stops after the shells whose strips are short (a quarter of them: ~6 % of the
+        // strip rows); they feed the DAG for the first ~30 ms of the upload
+        const int tend = (phase == 0 && !safe_order) ? std::min(T, (T / 4 + kG - 1) / kG * kG) : T;
+        for (int tlo = next_tlo; tlo < tend; tlo += kG) {
             const int thi = std::min(tlo + kG, T);
             const int rlo = std::max(0, M - thi);  // tile rows [rlo, M-1-tlo] (A, C), if tlo < M
             const size_t R0 = PL.rc[rlo];
@@ -968,6 +1002,10 @@ static int solve_host_pipelined(rsylv_b200_ctx* ctx, const SolveArgs& H, double*
                 launch_set_ready(Q.in_ready, t < M ? t + 1 : -1, t < N ? t + 1 : -1, t + 1, ss);
             }
         }
+        next_tlo = std::max(next_tlo, tend);
+        if (next_tlo < T) return;   // (phase 0 of the split order: the rest follows the DAG launch)
+        if (phase == 0 && !safe_order) return;  // everything fitted into phase 0: finish in phase 1
+        side_done = true;
         if (dbg) {  // (read after the solve: nothing here may block the host before the DAG launch)
             if (!dbg2) cudaEventCreate(&dbg2);
             if (!h_next) cudaMallocHost(&h_next, sizeof(int));
@@ -992,6 +1030,15 @@ static int solve_host_pipelined(rsylv_b200_ctx* ctx, const SolveArgs& H, double*
         std::fprintf(stderr, "[rsylv_b200] host pipeline: H2D copies %.1f ms for %.2f GB (%.1f GB/s); last shell "
                      "packed at %.1f ms, %d of %d tile tasks taken by then\n", ms, h2d / 1e9, h2d / 1e6 / ms, ms2,
                      *h_next, Q.ntasks);
+        if (g_dbg_a) {
+            float t0 = 0, t1 = 0, t2 = 0;
+            cudaEventSynchronize(ctx->evd);
+            cudaEventElapsedTime(&t0, ctx->evp, g_dbg_a);
+            cudaEventElapsedTime(&t1, g_dbg_a, g_dbg_b);
+            cudaEventElapsedTime(&t2, g_dbg_b, ctx->evd);
+            std::fprintf(stderr, "[rsylv_b200] host pipeline: main DAG kernel starts %.1f ms after the solve's setup, "
+                         "runs %.1f ms, the side stream's DAG CTAs end %.1f ms later\n", t0, t1, t2);
+        }
     }
     if (status != RSYLV_OK) return status;
     const int ae = alpha_exponent(emin, numax, PL.omega);
