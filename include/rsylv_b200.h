@@ -65,9 +65,10 @@ typedef struct {
     int virtual_ranks; /* >1: emulate that many GPUs on this device (tile columns block-cyclic,
                           solved tiles pushed between per-rank workspaces) -- validates the
                           multi-GPU exchange on one GPU; 0/1 = off                          */
-    int host_pipeline; /* rsylv_b200_solve only: stream the inputs in (H2D + pack per tile
-                          column) while the solve runs. 0: automatic (from 64 tiles),
-                          1: always, -1: never (copy everything first)                     */
+    int host_pipeline; /* rsylv_b200_solve only: stream the inputs in while the solve runs
+                          (H2D + pack in shells: tile row of A from its diagonal on, tile
+                          column of B, the matching L-shaped piece of C). 0: automatic (from
+                          64 tiles), 1: always, -1: never (copy everything first)          */
     int fast_diag;     /* diagonal-tile solves: 0 (default) = the exact exponent-form sub-block
                           path; 1 = a plain-FP64 attempt on the power-of-two normalized tile
                           first (tiles of 1x1 blocks), the exact path only when a pivot /
