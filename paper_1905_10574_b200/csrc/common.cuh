@@ -28,8 +28,14 @@ constexpr int kLDT = kBM + 1;    // shared-memory tile leading dim (odd: conflic
 constexpr int kLDD = kSub + 1;   // staged diagonal sub-block of B leading dim (column reads across lanes)
 constexpr int kLDDA = kSub;      // staged diagonal sub-block of A: row reads across lanes (r0 + 16 c: distinct banks)
 constexpr int kMaxRanks = 8;     // GPUs (or virtual ranks) sharing one solve
-constexpr int kKC = 32;          // K depth of one pipeline stage
-constexpr int kStages = 3;       // cp.async pipeline depth
+#ifndef RSYLV_KC
+#define RSYLV_KC 32
+#endif
+#ifndef RSYLV_STAGES
+#define RSYLV_STAGES 3
+#endif
+constexpr int kKC = RSYLV_KC;          // K depth of one pipeline stage (a multiple of 8)
+constexpr int kStages = RSYLV_STAGES;  // depth of the TMA operand ring
 constexpr int kThreads = 512;    // 16 warps, for both task kinds
 constexpr int kWarps = kThreads / 32;
 constexpr int kYNormExp = 500;   // solved Y tiles are stored with norm in [2^499, 2^500)
