@@ -30,3 +30,5 @@ for name in sys.argv[1:] or ["c1"]:
     print(name, "dag_ms", round(res.dag_ms, 2), "tiles", ntiles, " ".join(
         f"{names[i]}={out[i] / ntiles / 1965:.1f}us({100 * out[i] / tot:.0f}%)" for i in range(5)))
     print("   lookahead-ready sources %d, of which the flag was NOT set at the duty thread's own acquire: %d" % (out[26], out[25]))
+    if out[28] and out[31]:
+        print("   exact wavefront: urgent update %.2f us per solver warp and step; deferred updates %.2f us per idle warp and step (longest %.1f us)" % (out[30] / out[31] / 1965, out[27] / out[28] / 1965, out[29] / 1965))
