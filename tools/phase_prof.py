@@ -32,3 +32,5 @@ for name in sys.argv[1:] or ["c1"]:
     print("   lookahead-ready sources %d, of which the flag was NOT set at the duty thread's own acquire: %d" % (out[26], out[25]))
     if out[28] and out[31]:
         print("   exact wavefront: urgent update %.2f us per solver warp and step; deferred updates %.2f us per idle warp and step (longest %.1f us)" % (out[30] / out[31] / 1965, out[27] / out[28] / 1965, out[29] / 1965))
+    if out[22] and not out[14]:
+        print("   in-tile update sections (all calls, per call): bounds + destination load %.2f us, column product %.2f us, row product %.2f us, store %.2f us (%d calls)" % tuple([out[k] / out[22] / 1965 for k in (16, 17, 20, 21)] + [out[22]]))
