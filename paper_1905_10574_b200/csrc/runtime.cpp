@@ -877,12 +877,13 @@ int rsylv_b200_solve_device(rsylv_b200_ctx* ctx, size_t m, size_t n, const doubl
 }
 
 // Host pipeline (rsylv_b200_options.host_pipeline): the DAG starts on all but kPipeReserve SMs
-// while a side stream copies the inputs tile column by tile column -- A from the right, B and
-// C from the left, the order in which the anti-diagonal task list consumes them -- packs each
-// column on the reserved SMs, checks its tile norms on the device (the reference's argument
-// checks and reason order; a failure aborts the DAG and returns RSYLV_INVALID_ARGUMENT) and
-// publishes its count (tile tasks wait on these counters at their start); finally it launches
-// the remaining DAG CTAs, which join the task queue. Overlaps the H2D traffic with the solve.
+// while a copy stream uploads the inputs in shells (shell t: tile row M-1-t of A from its
+// diagonal tile on, tile column t of B, the matching L-shaped piece of C -- what the tiles with
+// max(M-1-i, j) == t need beyond the earlier shells) and a side stream packs each shell on the
+// reserved SMs, checks its tile norms on the device (the reference's argument checks and reason
+// order; a failure aborts the DAG and returns RSYLV_INVALID_ARGUMENT) and publishes the shell
+// count (tile tasks wait on these counters at their start); finally it launches the remaining
+// DAG CTAs, which join the task queue. Overlaps the H2D traffic with the solve.
 static int solve_host_pipelined(rsylv_b200_ctx* ctx, const SolveArgs& H, double* da, double* db,
                                 double* dc, double* dy) {
     cudaStream_t st = H.st;
