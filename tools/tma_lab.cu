@@ -94,6 +94,24 @@ __global__ void __launch_bounds__(512, 1) k_lab(const __grid_constant__ CUtensor
             if (v != e) ++nbad;
         }
     }
+    // the addressing update_phase uses: the four k of a DMMA step are {0, 1, 4, 5} (step 0) and
+    // {2, 3, 6, 7} (step 1) of each group of eight, which makes the loads conflict-free
+    const int kq = (q & 1) + 4 * (q >> 1);
+    const unsigned pa[2] = {wm * 8192u + kq * 64 + ((g * 8) ^ ((2 * (q >> 1)) << 4)),
+                            wm * 8192u + (kq + 2) * 64 + ((g * 8) ^ ((1 + 2 * (q >> 1)) << 4))};
+    const unsigned pb[2] = {(wn * 32u + g) * 64 + ((kq * 8) ^ (s << 4)),
+                            (wn * 32u + g) * 64 + (((kq + 2) * 8) ^ (s << 4))};
+    for (int kk = 0; kk < 32; kk += 4) {
+        const int step = (kk >> 2) & 1, k = (kk >> 3) * 8 + 2 * step + kq;
+        for (int mi = 0; mi < 4; ++mi) {
+            const double v = *(const double*)(sL + pa[step] + mi * 2048 + (kk >> 3) * 512);
+            if (v != L[(wm * 32 + mi * 8 + g) + (size_t)(k0 + k) * 128]) ++nbad;
+        }
+        for (int ni = 0; ni < 4; ++ni) {
+            const double v = *(const double*)(sR + pb[step] + ni * 512 + (kk >> 3) * 8192);
+            if (v != R[(k0 + k) + (size_t)(wn * 32 + ni * 8 + g) * 128]) ++nbad;
+        }
+    }
     if (nbad) atomicAdd(bad, nbad);
 }
 
